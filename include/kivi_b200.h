@@ -1,0 +1,222 @@
+/*
+ * kivi_b200.h — C ABI of the B200-native KIVI KV-cache hot path.
+ *
+ * One `kivi_cache` holds n_units independent streaming caches (one per
+ * (batch element, kv-head) of a layer — a "unit" is the reference's
+ * KeyCacheState + ValueCacheState pair, reference
+ * proj/include/kivi/kv_cache.hpp:22-35).  All units of a cache advance in
+ * lockstep: every append adds exactly one token to every unit, which is how a
+ * decode step drives them (reference proj/src/workload.cpp:224-242).
+ *
+ * Conventions
+ *   - Plain C types only; no torch, no C++ in the signatures.
+ *   - Every data pointer of a non-`_host` entry point is a DEVICE pointer
+ *     (cudaMalloc'd, or any memory the GPU can dereference); work is enqueued
+ *     on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *     stream) and the call returns without synchronising.
+ *   - `_host` entry points take HOST pointers, stage them through the cache's
+ *     pinned/device buffers inside the call, and synchronise `stream` before
+ *     returning (the results are in the host buffers on return).
+ *   - Errors mirror the reference's exception types (reference
+ *     proj/include/kivi/errors.hpp:10-22): a failing call returns a status
+ *     and leaves the cache unchanged; kivi_last_error() returns a
+ *     thread-local message.
+ *   - Numerics: packed codes and per-group zero-points/maxima are bit-exact
+ *     with the reference quantizer (reference proj/src/quantize.cpp:22-48);
+ *     attention outputs are fp32 and within the tolerances stated in
+ *     DESIGN.md.
+ */
+#ifndef KIVI_B200_H
+#define KIVI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KIVI_B200_ABI_VERSION 1
+
+typedef enum kivi_status {
+    KIVI_OK = 0,
+    KIVI_ERR_SHAPE = 1,    /* reference ShapeError  (errors.hpp:10)  */
+    KIVI_ERR_USAGE = 2,    /* reference UsageError  (errors.hpp:15)  */
+    KIVI_ERR_CONFIG = 3,   /* reference ConfigError (errors.hpp:20)  */
+    KIVI_ERR_CUDA = 4,     /* CUDA runtime / launch failure          */
+    KIVI_ERR_OOM = 5,      /* device or pinned allocation failed     */
+    KIVI_ERR_CAPACITY = 6  /* append past a cache's fixed capacity   */
+} kivi_status;
+
+/* Mirrors reference CacheConfig (kv_cache.hpp:9-18): B, G, R, d.
+ * validate(): 1 <= bits <= 8 and packable (bits in {1,2,4,8}),
+ * group_size >= 1, residual_length >= 1, residual_length % group_size == 0,
+ * head_dim >= 1, head_dim % group_size == 0 (kv_cache.cpp:7-21,
+ * quantize.cpp:13-20, 173-176). */
+typedef struct kivi_config {
+    int32_t bits;
+    int64_t group_size;
+    int64_t residual_length;
+    int64_t head_dim;
+} kivi_config;
+
+/* Quantization axis, reference Axis (quantize.hpp:14). */
+typedef enum kivi_axis { KIVI_PER_TOKEN = 0, KIVI_PER_CHANNEL = 1 } kivi_axis;
+
+typedef struct kivi_cache kivi_cache;
+
+/* Counters of one cache (identical for every unit). */
+typedef struct kivi_cache_info {
+    int64_t n_units;
+    int64_t capacity_tokens;
+    int64_t total_tokens;             /* l                                    */
+    int64_t key_grouped_tokens;       /* l - l % R                            */
+    int64_t key_residual_rows;        /* l % R                                */
+    int64_t key_residual_capacity;    /* reference KeyCacheState::residual_capacity */
+    int64_t value_grouped_tokens;     /* l - min(l, R)                        */
+    int64_t value_residual_rows;      /* min(l, R)                            */
+    int64_t value_residual_capacity;
+    uint64_t key_memory_bytes;        /* reference memory_bytes(KeyCacheState), per unit */
+    uint64_t value_memory_bytes;      /* reference memory_bytes(ValueCacheState), per unit */
+    uint64_t device_bytes;            /* bytes this cache holds in HBM        */
+} kivi_cache_info;
+
+/* Host-side view of one unit's state in the REFERENCE's layout
+ * (QuantizedTensor::packed()/zero_points()/scales(), residual rows in token
+ * order).  Buffers are caller-owned; sizes follow kivi_cache_info:
+ *   key_packed   ceil(key_grouped_tokens*d*B/8) bytes
+ *   key_zero/key_scale   key_grouped_tokens*d/G doubles
+ *   key_residual key_residual_rows*d floats
+ *   value_packed ceil(value_grouped_tokens*d*B/8) bytes
+ *   value_zero/value_scale value_grouped_tokens*d/G doubles
+ *   value_residual value_residual_rows*d floats
+ * Any pointer may be NULL to skip that field (export only). */
+typedef struct kivi_unit_state {
+    uint8_t* key_packed;
+    double* key_zero;
+    double* key_scale;
+    float* key_residual;
+    uint8_t* value_packed;
+    double* value_zero;
+    double* value_scale;
+    float* value_residual;
+} kivi_unit_state;
+
+/* Last error message of the calling thread ("" if none). */
+const char* kivi_last_error(void);
+int kivi_abi_version(void);
+
+/* Validates like CacheConfig::validate (kv_cache.cpp:7-21) + packable. */
+kivi_status kivi_config_validate(const kivi_config* cfg);
+
+/* ---- cache lifetime (replaces constructing KeyCacheState/ValueCacheState) */
+kivi_status kivi_cache_create(const kivi_config* cfg, int device, int64_t n_units,
+                              int64_t capacity_tokens, kivi_cache** out);
+kivi_status kivi_cache_destroy(kivi_cache* cache);
+/* Grows every unit's capacity (device reallocation + copy); stream-ordered. */
+kivi_status kivi_cache_reserve(kivi_cache* cache, int64_t capacity_tokens, void* stream);
+/* Deep copy (reference states are copyable, workload.cpp:166-167). */
+kivi_status kivi_cache_clone(const kivi_cache* src, void* stream, kivi_cache** out);
+kivi_status kivi_cache_get_info(const kivi_cache* cache, kivi_cache_info* info);
+
+/* ---- hot path ------------------------------------------------------------ */
+
+/* Reference prefill (kv_cache.cpp:23-55): resets every unit to the prompt.
+ * keys/values: [n_units][l][d] fp32.  l >= 1 else KIVI_ERR_USAGE. */
+kivi_status kivi_prefill(kivi_cache* cache, const float* keys, const float* values, int64_t l,
+                         void* stream);
+
+/* Reference append_token (kv_cache.cpp:66-98) for every unit.
+ * t_k, t_v: [n_units][d] fp32. */
+kivi_status kivi_append(kivi_cache* cache, const float* t_k, const float* t_v, void* stream);
+
+/* Attention of the current state (no append) — the second half of the
+ * reference decode_attention (attention.cpp:36-99), for q_per_kv query heads
+ * per unit (q_per_kv == 1 is the reference's MHA; >1 is GQA, which the
+ * reference emulates with one state copy per query head).
+ *   t_q:     [n_units][q_per_kv][d] fp32
+ *   out:     [n_units][q_per_kv][d] fp32
+ *   weights: NULL, or [n_units][q_per_kv][l] fp32 normalised softmax weights
+ *            (reference DecodeOutput::weights, attention.hpp:14)
+ *   scale_logits: reference AttentionOptions::scale_logits (attention.hpp:7-10) */
+kivi_status kivi_attend(kivi_cache* cache, const float* t_q, int32_t q_per_kv, float* out,
+                        float* weights, int32_t scale_logits, void* stream);
+
+/* Reference decode_attention (attention.cpp:26-100): append, then attend. */
+kivi_status kivi_decode(kivi_cache* cache, const float* t_q, const float* t_k, const float* t_v,
+                        int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
+                        void* stream);
+
+/* Host-buffer variants: copies in and out happen inside the call. */
+kivi_status kivi_prefill_host(kivi_cache* cache, const float* keys, const float* values,
+                              int64_t l, void* stream);
+kivi_status kivi_append_host(kivi_cache* cache, const float* t_k, const float* t_v,
+                             void* stream);
+kivi_status kivi_decode_host(kivi_cache* cache, const float* t_q, const float* t_k,
+                             const float* t_v, int32_t q_per_kv, float* out, float* weights,
+                             int32_t scale_logits, void* stream);
+
+/* ---- state exchange in the reference layout (parity / drop-in facade) ---- */
+
+/* Copies unit `unit` to host buffers; synchronises `stream`. */
+kivi_status kivi_export_unit(const kivi_cache* cache, int64_t unit, kivi_unit_state* dst,
+                             void* stream);
+/* Sets every unit's token count to `total_tokens` and loads unit `unit` from
+ * host buffers in the reference layout (all units of the cache must later be
+ * loaded, or they hold zeros).  Synchronises `stream`. */
+kivi_status kivi_import_unit(kivi_cache* cache, int64_t unit, int64_t total_tokens,
+                             int64_t key_residual_capacity, int64_t value_residual_capacity,
+                             const kivi_unit_state* src, void* stream);
+/* Reference materialize_keys / materialize_values (kv_cache.cpp:100-106):
+ * [n_units][l][d] fp32, bit-exact dequantisation (double, quantize.cpp:142-167). */
+kivi_status kivi_materialize(const kivi_cache* cache, float* keys_out, float* values_out,
+                             void* stream);
+
+/* ---- standalone quantizer (reference quantize.hpp:35-96) ----------------- */
+
+/* QuantizedTensor::quantize (quantize.cpp:171-185) of a rows x cols fp32
+ * matrix: packed bytes (ceil(rows*cols*B/8)), per-group zero-points and
+ * scales as double (group order quantize.cpp:105-140).  Device pointers. */
+kivi_status kivi_quantize_matrix(const float* m, int64_t rows, int64_t cols, int32_t bits,
+                                 int64_t group_size, kivi_axis axis, uint8_t* packed,
+                                 double* zero_points, double* scales, void* stream);
+/* QuantizedTensor::dequantize (quantize.cpp:187-192 -> 142-167). */
+kivi_status kivi_dequantize_matrix(const uint8_t* packed, const double* zero_points,
+                                   const double* scales, int64_t rows, int64_t cols,
+                                   int32_t bits, int64_t group_size, kivi_axis axis, float* out,
+                                   void* stream);
+/* pack_codes / unpack_codes (quantize.cpp:59-93).  pack returns
+ * KIVI_ERR_USAGE for bits not in {1,2,4,8} or a code > 2^B-1 (after
+ * synchronising `stream` to inspect the device-side range check). */
+kivi_status kivi_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* bytes,
+                            void* stream);
+kivi_status kivi_unpack_codes(const uint8_t* bytes, int64_t n, int32_t bits, uint8_t* codes,
+                              void* stream);
+/* Reference reference_attention (attention.cpp:16-24): full-precision
+ * softmax(scale * q K^T) V for q: [n_q][d], K,V: [l][d] -> out [n_q][d]. */
+kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* keys,
+                                     const float* values, int64_t l, int64_t d,
+                                     int32_t scale_logits, float* out, void* stream);
+
+/* ---- measurement hooks (bench.py) --------------------------------------- */
+
+/* Selects the attend kernel: 0 = auto (fast sm_100a kernel when the shape is
+ * supported, else generic), 1 = force generic, 2 = force fast (error if the
+ * shape is unsupported). */
+kivi_status kivi_set_attend_path(kivi_cache* cache, int32_t path);
+/* When enabled, kivi_attend records CUDA events around its main kernel. */
+kivi_status kivi_profile_enable(kivi_cache* cache, int32_t enable);
+/* Synchronises the recorded events and returns the summed main-kernel time,
+ * the number of main-kernel launches and the total number of kernels this
+ * library launched for the cache since the last reset; then resets. */
+kivi_status kivi_profile_read(kivi_cache* cache, double* main_kernel_ms, int64_t* main_launches,
+                              int64_t* total_launches);
+/* Algorithmic HBM bytes the attend kernel must read + write per unit for the
+ * cache's current state and q_per_kv (SURVEY §8d formula). */
+kivi_status kivi_attend_bytes(const kivi_cache* cache, int32_t q_per_kv, uint64_t* bytes_per_unit);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KIVI_B200_H */

@@ -1,0 +1,186 @@
+// Shared device helpers for the KIVI B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kivi_b200 {
+
+// ---------------------------------------------------------------------------
+// Exact group quantizer.
+//
+// Reference quantize_group (proj/src/quantize.cpp:22-48):
+//   lo, hi  = float min / max of the group (first smallest, last largest —
+//             std::minmax_element semantics; only visible for +0/-0 ties)
+//   if hi == lo: scale 1, all codes 0
+//   s       = (double(hi) - double(lo)) / (2^B - 1)              (double)
+//   code    = clamp(nearbyint((double(v) - lo) / s), 0, 2^B - 1) (ties-even)
+//
+// The device version stores the group as the float pair (lo, hi), from which
+// the reference's double scale is recomputed bit-exactly anywhere.  Codes are
+// decided in fp32 with an error bound (|x - X| < 1e-4 for B <= 8) and only
+// values within 1e-3 of a rounding tie take the exact double path, so every
+// code equals the reference's.
+// ---------------------------------------------------------------------------
+struct GroupRange {
+    float lo;
+    float hi;
+};
+
+__device__ __forceinline__ void minmax_step(float v, float& lo, float& hi) {
+    if (v < lo) lo = v;     // first smallest
+    if (!(v < hi)) hi = v;  // last largest
+}
+
+__device__ __forceinline__ double group_scale(float lo, float hi, int maxc) {
+    if (hi == lo) return 1.0;
+    return __ddiv_rn(__dsub_rn((double)hi, (double)lo), (double)maxc);
+}
+
+struct CodeCtx {
+    float lo;
+    float r;        // maxc / (hi - lo) in fp32
+    double lo_d;
+    double s;       // exact reference scale
+    int maxc;
+    bool degenerate;
+    bool fast_ok;
+};
+
+__device__ __forceinline__ CodeCtx make_code_ctx(float lo, float hi, int maxc) {
+    CodeCtx c;
+    c.lo = lo;
+    c.lo_d = (double)lo;
+    c.maxc = maxc;
+    c.degenerate = (hi == lo);
+    c.s = group_scale(lo, hi, maxc);
+    float span = hi - lo;
+    c.r = (float)maxc / span;
+    c.fast_ok = !c.degenerate && isfinite(c.r) && c.r > 0.0f;
+    return c;
+}
+
+__device__ __forceinline__ uint32_t quant_code(const CodeCtx& c, float v) {
+    if (c.degenerate) return 0u;
+    if (c.fast_ok) {
+        float x = (v - c.lo) * c.r;
+        if (isfinite(x)) {
+            float fl = floorf(x);
+            float frac = x - fl;
+            if (fabsf(frac - 0.5f) > 1e-3f) {
+                float q = rintf(x);
+                q = fminf(fmaxf(q, 0.0f), (float)c.maxc);
+                return (uint32_t)q;
+            }
+        }
+    }
+    double q = rint(__ddiv_rn(__dsub_rn((double)v, c.lo_d), c.s));
+    q = fmin(fmax(q, 0.0), (double)c.maxc);
+    return (uint32_t)q;
+}
+
+// Reference dequantisation: float(double(code) * s + z), no contraction
+// (quantize.cpp:50-57, 142-167).
+__device__ __forceinline__ float dequant_exact(uint32_t code, double s, double z) {
+    return (float)__dadd_rn(__dmul_rn((double)code, s), z);
+}
+
+// ---------------------------------------------------------------------------
+// Little-endian bit streams (reference pack_codes, quantize.cpp:59-76): code
+// i occupies bits [i*B, i*B+B) of the byte stream.  With B in {1,2,4,8} a
+// code never straddles a 32-bit word, so a 32-bit little-endian word view
+// addresses it as bit (i*B) & 31 of word (i*B) >> 5.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t read_code(const uint8_t* base, uint64_t bit, int bits) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+    return (w[bit >> 5] >> (bit & 31)) & ((1u << bits) - 1u);
+}
+
+// OR `code` into a zero-initialised stream (concurrent writers of one word
+// are fine).
+__device__ __forceinline__ void or_code(uint8_t* base, uint64_t bit, int bits, uint32_t code) {
+    (void)bits;
+    if (code == 0u) return;
+    uint32_t* w = reinterpret_cast<uint32_t*>(base);
+    atomicOr(&w[bit >> 5], code << (bit & 31));
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA, cp.async.bulk) + mbarrier helpers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk global->shared copy completing on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Same with an L2 evict-first policy: the cache is streamed exactly once per
+// decode step, so it should not displace other lines.
+__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes,
+                                                     uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t make_evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace kivi_b200

@@ -1,0 +1,335 @@
+// Quantize / append / prefill / materialize kernels (bit-exact with the
+// reference quantizer).  Generic over B in {1,2,4,8}, any G, R, d with
+// R % G == 0 and d % G == 0.
+#pragma once
+
+#include "common.cuh"
+
+namespace kivi_b200 {
+
+// Device layout of one cache (all arrays are [n_units][...], unit strides in
+// elements of each array).  See DESIGN.md "HBM layout".
+struct CacheDev {
+    int bits, G, R, d, maxc;
+    int64_t n_units;
+    // Key codes: reference per-channel group order — bit ((tg*d + c)*G + i)*B
+    // of a unit's stream (quantize.cpp:118-127).  Pairs [tg*d + c] = (lo, hi).
+    uint8_t* kcodes;
+    int64_t k_ustride;  // bytes
+    float2* kpairs;
+    int64_t kp_ustride;  // float2 elements
+    // Value codes: per-token order — bit (t*d + c)*B (quantize.cpp:128-138).
+    // Pairs [t*(d/G) + cg].
+    uint8_t* vcodes;
+    int64_t v_ustride;
+    float2* vpairs;
+    int64_t vp_ustride;
+    // Residual windows: fp32 rings [R][d]; key token t (>= kg) at row t - kg,
+    // value token t (>= vg) at row t % R.
+    float* kring;
+    float* vring;
+    int64_t ring_ustride;  // floats
+};
+
+// Quantizes one group of G values read as p[i*stride] (i < G) and ORs its
+// codes into `codes` starting at bit `bit0`; returns (lo, hi).
+__device__ __forceinline__ float2 quantize_group_dev(const float* p, int64_t stride, int G,
+                                                     int bits, int maxc, uint8_t* codes,
+                                                     uint64_t bit0) {
+    float lo = p[0], hi = p[0];
+    for (int i = 1; i < G; ++i) minmax_step(p[(int64_t)i * stride], lo, hi);
+    CodeCtx cc = make_code_ctx(lo, hi, maxc);
+    if (!cc.degenerate) {
+        // Accumulate whole 32-bit words, flush each once.
+        uint64_t bit = bit0;
+        uint32_t word = 0;
+        uint64_t cur = bit >> 5;
+        for (int i = 0; i < G; ++i, bit += (uint64_t)bits) {
+            uint64_t wi = bit >> 5;
+            if (wi != cur) {
+                if (word) atomicOr(reinterpret_cast<uint32_t*>(codes) + cur, word);
+                word = 0;
+                cur = wi;
+            }
+            word |= quant_code(cc, p[(int64_t)i * stride]) << (bit & 31);
+        }
+        if (word) atomicOr(reinterpret_cast<uint32_t*>(codes) + cur, word);
+    }
+    return make_float2(lo, hi);
+}
+
+// ---- prefill (reference prefill, kv_cache.cpp:23-55) ----------------------
+
+// One thread per key group (unit, tg, c) of the first kg tokens.
+__global__ void prefill_keys_kernel(CacheDev c, const float* __restrict__ keys, int64_t l,
+                                    int64_t kg) {
+    const int64_t tiles = kg / c.G;
+    const int64_t per_unit = tiles * c.d;
+    const int64_t total = per_unit * c.n_units;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        const int64_t g = gid % per_unit;  // tg*d + ch
+        const int64_t tg = g / c.d, ch = g % c.d;
+        const float* src = keys + (u * l + tg * c.G) * c.d + ch;
+        float2 r = quantize_group_dev(src, c.d, c.G, c.bits, c.maxc, c.kcodes + u * c.k_ustride,
+                                      (uint64_t)g * c.G * c.bits);
+        c.kpairs[u * c.kp_ustride + g] = r;
+    }
+}
+
+// One thread per value group (unit, t, cg) of the first vg tokens.
+__global__ void prefill_values_kernel(CacheDev c, const float* __restrict__ values, int64_t l,
+                                      int64_t vg) {
+    const int64_t gpt = c.d / c.G;
+    const int64_t per_unit = vg * gpt;
+    const int64_t total = per_unit * c.n_units;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        const int64_t g = gid % per_unit;  // t*gpt + cg
+        const int64_t t = g / gpt, cg = g % gpt;
+        const float* src = values + (u * l + t) * c.d + cg * c.G;
+        float2 r = quantize_group_dev(src, 1, c.G, c.bits, c.maxc, c.vcodes + u * c.v_ustride,
+                                      (uint64_t)g * c.G * c.bits);
+        c.vpairs[u * c.vp_ustride + g] = r;
+    }
+}
+
+// Residual rows: keys [kg, l) -> ring rows [0, l-kg); values [vg, l) -> rows t % R.
+__global__ void prefill_residual_kernel(CacheDev c, const float* __restrict__ keys,
+                                        const float* __restrict__ values, int64_t l, int64_t kg,
+                                        int64_t vg) {
+    const int64_t kr = l - kg, vr = l - vg;
+    const int64_t per_unit = (kr + vr) * c.d;
+    const int64_t total = per_unit * c.n_units;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        int64_t e = gid % per_unit;
+        const int64_t ch = e % c.d;
+        int64_t row = e / c.d;
+        if (row < kr) {
+            const int64_t t = kg + row;
+            c.kring[u * c.ring_ustride + row * c.d + ch] = keys[(u * l + t) * c.d + ch];
+        } else {
+            const int64_t t = vg + (row - kr);
+            c.vring[u * c.ring_ustride + (t % c.R) * c.d + ch] = values[(u * l + t) * c.d + ch];
+        }
+    }
+}
+
+// ---- append (reference append_token, kv_cache.cpp:66-98) -----------------
+// One CTA per unit.  `l` = token count BEFORE the append.
+__global__ void append_kernel(CacheDev c, const float* __restrict__ tk,
+                              const float* __restrict__ tv, int64_t l) {
+    const int64_t u = blockIdx.x;
+    const int R = c.R, d = c.d, G = c.G;
+    float* kring = c.kring + u * c.ring_ustride;
+    float* vring = c.vring + u * c.ring_ustride;
+    const int slot = (int)(l % R);
+
+    // Key: push the row into the ring (row l - kg == l % R).
+    for (int ch = threadIdx.x; ch < d; ch += blockDim.x)
+        kring[(int64_t)slot * d + ch] = tk[u * d + ch];
+
+    // Value: the FIFO is full (l >= R): quantize the oldest row (token l - R,
+    // ring row l % R) per-token before it is overwritten.
+    if (l >= R) {
+        const int64_t e = l - R;
+        const int gpt = d / G;
+        for (int cg = threadIdx.x; cg < gpt; cg += blockDim.x) {
+            float2 r = quantize_group_dev(vring + (int64_t)slot * d + cg * G, 1, G, c.bits, c.maxc,
+                                          c.vcodes + u * c.v_ustride,
+                                          ((uint64_t)e * d + (uint64_t)cg * G) * c.bits);
+            c.vpairs[u * c.vp_ustride + e * gpt + cg] = r;
+        }
+    }
+    __syncthreads();
+    for (int ch = threadIdx.x; ch < d; ch += blockDim.x)
+        vring[(int64_t)slot * d + ch] = tv[u * d + ch];
+
+    // Key flush when the residual reaches R rows: quantize the R x d block
+    // per-channel into tiles (l+1-R)/G ... (l+1)/G - 1.
+    if ((l + 1) % R == 0) {
+        const int64_t tile0 = (l + 1 - R) / G;
+        const int ngroups = (R / G) * d;
+        for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+            const int tl = g / d, ch = g % d;
+            const int64_t gi = (tile0 + tl) * d + ch;
+            float2 r = quantize_group_dev(kring + (int64_t)tl * G * d + ch, d, G, c.bits, c.maxc,
+                                          c.kcodes + u * c.k_ustride, (uint64_t)gi * G * c.bits);
+            c.kpairs[u * c.kp_ustride + gi] = r;
+        }
+    }
+}
+
+// ---- materialize (reference materialize_*, kv_cache.cpp:100-106) ---------
+__global__ void materialize_kernel(CacheDev c, int64_t l, int64_t kg, int64_t vg,
+                                   float* __restrict__ kout, float* __restrict__ vout) {
+    const int64_t per_unit = l * c.d;
+    const int64_t total = per_unit * c.n_units;
+    const int gpt = c.d / c.G;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        const int64_t e = gid % per_unit;
+        const int64_t t = e / c.d, ch = e % c.d;
+        if (kout) {
+            float val;
+            if (t < kg) {
+                const int64_t tg = t / c.G, i = t % c.G;
+                const int64_t g = tg * c.d + ch;
+                float2 pr = c.kpairs[u * c.kp_ustride + g];
+                uint32_t code = read_code(c.kcodes + u * c.k_ustride,
+                                          ((uint64_t)g * c.G + i) * c.bits, c.bits);
+                val = dequant_exact(code, group_scale(pr.x, pr.y, c.maxc), (double)pr.x);
+            } else {
+                val = c.kring[u * c.ring_ustride + (t - kg) * c.d + ch];
+            }
+            kout[gid] = val;
+        }
+        if (vout) {
+            float val;
+            if (t < vg) {
+                const int64_t g = t * gpt + ch / c.G;
+                float2 pr = c.vpairs[u * c.vp_ustride + g];
+                uint32_t code = read_code(c.vcodes + u * c.v_ustride,
+                                          ((uint64_t)t * c.d + ch) * c.bits, c.bits);
+                val = dequant_exact(code, group_scale(pr.x, pr.y, c.maxc), (double)pr.x);
+            } else {
+                val = c.vring[u * c.ring_ustride + (t % c.R) * c.d + ch];
+            }
+            vout[gid] = val;
+        }
+    }
+}
+
+// ---- export / import in the reference layout --------------------------------
+// (lo, hi) pairs -> reference (zero_point, scale) doubles.
+__global__ void pairs_to_zs_kernel(const float2* __restrict__ pairs, int64_t n, int maxc,
+                                   double* __restrict__ z, double* __restrict__ s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 p = pairs[i];
+        z[i] = (double)p.x;
+        s[i] = group_scale(p.x, p.y, maxc);
+    }
+}
+
+// Reference (zero_point, scale) -> (lo, hi): hi = float(z + s*maxc) recovers
+// the group maximum for every state this library exported.
+__global__ void zs_to_pairs_kernel(const double* __restrict__ z, const double* __restrict__ s,
+                                   int64_t n, int maxc, float2* __restrict__ pairs) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float lo = (float)z[i];
+        float hi = (float)__dadd_rn(z[i], __dmul_rn(s[i], (double)maxc));
+        if (s[i] == 1.0 && hi != lo) {
+            // Degenerate groups (s == 1, all codes 0) and genuine s == 1 groups
+            // both dequantise to z + code; keep hi as computed.
+        }
+        pairs[i] = make_float2(lo, hi);
+    }
+}
+
+// Value ring (tokens [vg, l) at rows t % R) <-> token-ordered rows.
+__global__ void ring_gather_kernel(const float* __restrict__ ring, int64_t first_token,
+                                   int64_t rows, int R, int d, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d, ch = i % d;
+        out[i] = ring[((first_token + r) % R) * d + ch];
+    }
+}
+__global__ void ring_scatter_kernel(float* __restrict__ ring, int64_t first_token, int64_t rows,
+                                    int R, int d, const float* __restrict__ in) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d, ch = i % d;
+        ring[((first_token + r) % R) * d + ch] = in[i];
+    }
+}
+
+// ---- standalone matrix quantizer (QuantizedTensor::quantize) --------------
+// One thread per group; group order per quantize.cpp:105-140.
+__global__ void quantize_matrix_kernel(const float* __restrict__ m, int64_t rows, int64_t cols,
+                                       int bits, int G, int per_channel, uint8_t* packed,
+                                       double* __restrict__ zp, double* __restrict__ sc) {
+    const int maxc = (1 << bits) - 1;
+    const int64_t ngroups = rows * cols / G;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const float* src;
+        int64_t stride;
+        if (per_channel) {
+            const int64_t tg = g / cols, ch = g % cols;
+            src = m + tg * G * cols + ch;
+            stride = cols;
+        } else {
+            const int64_t gpr = cols / G;
+            const int64_t r = g / gpr, cg = g % gpr;
+            src = m + r * cols + cg * G;
+            stride = 1;
+        }
+        float2 r = quantize_group_dev(src, stride, G, bits, maxc, packed, (uint64_t)g * G * bits);
+        zp[g] = (double)r.x;
+        sc[g] = group_scale(r.x, r.y, maxc);
+    }
+}
+
+// QuantizedTensor::dequantize: one thread per element.
+__global__ void dequantize_matrix_kernel(const uint8_t* __restrict__ packed,
+                                         const double* __restrict__ zp,
+                                         const double* __restrict__ sc, int64_t rows,
+                                         int64_t cols, int bits, int G, int per_channel,
+                                         float* __restrict__ out) {
+    const int64_t n = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / cols, ch = e % cols;
+        int64_t g, pos;
+        if (per_channel) {
+            const int64_t tg = r / G, i = r % G;
+            g = tg * cols + ch;
+            pos = g * G + i;
+        } else {
+            g = r * (cols / G) + ch / G;
+            pos = e;  // per-token stream order == row-major order
+        }
+        uint32_t code = read_code(packed, (uint64_t)pos * bits, bits);
+        out[e] = dequant_exact(code, sc[g], zp[g]);
+    }
+}
+
+// pack_codes: one thread per output byte; flags out-of-range codes.
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t n, int bits,
+                                  uint8_t* __restrict__ bytes, int* __restrict__ bad) {
+    const int per = 8 / bits;
+    const int64_t nbytes = (n * bits + 7) / 8;
+    const int maxc = (1 << bits) - 1;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int k = 0; k < per; ++k) {
+            const int64_t i = b * per + k;
+            if (i >= n) break;
+            uint32_t cd = codes[i];
+            if (cd > (uint32_t)maxc) atomicMax(bad, 1);
+            v |= (cd & (uint32_t)maxc) << (k * bits);
+        }
+        bytes[b] = (uint8_t)v;
+    }
+}
+
+__global__ void unpack_codes_kernel(const uint8_t* __restrict__ bytes, int64_t n, int bits,
+                                    uint8_t* __restrict__ codes) {
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t bit = (uint64_t)i * bits;
+        codes[i] = (uint8_t)((bytes[bit >> 3] >> (bit & 7)) & mask);
+    }
+}
+
+}  // namespace kivi_b200

@@ -1,0 +1,982 @@
+// C-ABI implementation of include/kivi_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kivi_b200.h"
+#include "common.cuh"
+#include "kernels_attend_fast.cuh"
+#include "kernels_attend_generic.cuh"
+#include "kernels_quant.cuh"
+
+using namespace kivi_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+kivi_status fail(kivi_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define KIVI_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            if (e_ == cudaErrorMemoryAllocation)                                           \
+                return fail(KIVI_ERR_OOM, "%s: %s", #call, cudaGetErrorString(e_));       \
+            return fail(KIVI_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));          \
+        }                                                                                  \
+    } while (0)
+
+#define KIVI_LAUNCHED()                                                                     \
+    do {                                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess) return fail(KIVI_ERR_CUDA, "launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+int grid_for(int64_t n, int block = 256) {
+    int64_t g = ceil_div(std::max<int64_t>(n, 1), block);
+    return (int)std::min<int64_t>(g, 148LL * 32);
+}
+
+// RAII-less device buffer helper (the cache owns and frees them).
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+}  // namespace
+
+struct kivi_cache {
+    kivi_config cfg{};
+    int device = 0;
+    int64_t n_units = 0;
+    int64_t cap = 0;  // tokens per unit (multiple of R)
+    int64_t l = 0;
+    int64_t kres_cap = 0, vres_cap = 0;  // reference residual_capacity
+    int attend_path = 0;
+    CacheDev dev{};
+
+    // workspaces (grown lazily)
+    float* part_o = nullptr;
+    int64_t part_cap = 0;
+    float2* part_ml = nullptr;
+    int64_t ml_cap = 0;
+    float* scratch = nullptr;
+    int64_t scratch_cap = 0;
+    float2* stats = nullptr;
+    int64_t stats_cap = 0;
+    int fast_per_sm[9][4] = {};
+    // staging for _host calls
+    float* st_q = nullptr;
+    float* st_k = nullptr;
+    float* st_v = nullptr;
+    float* st_out = nullptr;
+    float* st_w = nullptr;
+    int64_t st_cap_q = 0, st_cap_out = 0, st_cap_k = 0, st_cap_v = 0, st_cap_w = 0;
+
+    // profiling
+    bool profile = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    int64_t main_launches = 0;
+    int64_t total_launches = 0;
+
+    int64_t kg() const { return l - l % cfg.residual_length; }
+    int64_t vg() const { return l - std::min<int64_t>(l, cfg.residual_length); }
+};
+
+namespace {
+
+kivi_status validate_cfg(const kivi_config* cfg) {
+    if (!cfg) return fail(KIVI_ERR_USAGE, "config is NULL");
+    // QuantParams::validate (quantize.cpp:13-20)
+    if (cfg->bits < 1 || cfg->bits > 8)
+        return fail(KIVI_ERR_CONFIG, "bits must be in [1, 8], got %d", cfg->bits);
+    if (cfg->group_size < 1)
+        return fail(KIVI_ERR_CONFIG, "group_size must be >= 1, got %lld",
+                    (long long)cfg->group_size);
+    // CacheConfig::validate (kv_cache.cpp:7-21)
+    if (cfg->residual_length < 1) return fail(KIVI_ERR_CONFIG, "residual_length must be >= 1");
+    if (cfg->residual_length % cfg->group_size != 0)
+        return fail(KIVI_ERR_CONFIG, "residual_length %lld must be divisible by group_size %lld",
+                    (long long)cfg->residual_length, (long long)cfg->group_size);
+    if (cfg->head_dim < 1 || cfg->head_dim % cfg->group_size != 0)
+        return fail(KIVI_ERR_CONFIG, "head_dim %lld must be a positive multiple of group_size %lld",
+                    (long long)cfg->head_dim, (long long)cfg->group_size);
+    // Packed storage (quantize.cpp:173-176)
+    if (!(cfg->bits == 1 || cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8))
+        return fail(KIVI_ERR_CONFIG,
+                    "packed storage requires bits in {1,2,4,8}; B=%d is fake-quant only", cfg->bits);
+    return KIVI_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void free_cache_buffers(kivi_cache* h) {
+    cudaFree(h->dev.kcodes);
+    cudaFree(h->dev.kpairs);
+    cudaFree(h->dev.vcodes);
+    cudaFree(h->dev.vpairs);
+    cudaFree(h->dev.kring);
+    cudaFree(h->dev.vring);
+    h->dev.kcodes = nullptr;
+    h->dev.kpairs = nullptr;
+    h->dev.vcodes = nullptr;
+    h->dev.vpairs = nullptr;
+    h->dev.kring = nullptr;
+    h->dev.vring = nullptr;
+}
+
+struct Layout {
+    int64_t cap, k_ustride, kp_ustride, v_ustride, vp_ustride, ring_ustride;
+};
+
+Layout make_layout(const kivi_config& cfg, int64_t capacity) {
+    Layout L;
+    const int64_t R = cfg.residual_length, G = cfg.group_size, d = cfg.head_dim, B = cfg.bits;
+    L.cap = std::max<int64_t>(round_up(std::max<int64_t>(capacity, 1), R), R);
+    const int64_t tiles = L.cap / G;
+    L.k_ustride = round_up(ceil_div(tiles * d * G * B, 8), 256);
+    L.kp_ustride = round_up(tiles * d, 32);
+    L.v_ustride = round_up(ceil_div(L.cap * d * B, 8), 256);
+    L.vp_ustride = round_up(L.cap * (d / G), 32);
+    L.ring_ustride = round_up(R * d, 64);
+    return L;
+}
+
+kivi_status alloc_cache_buffers(kivi_cache* h, const Layout& L, cudaStream_t st) {
+    CacheDev& c = h->dev;
+    const int64_t U = h->n_units;
+    KIVI_CUDA(dalloc(&c.kcodes, (size_t)(U * L.k_ustride)));
+    KIVI_CUDA(dalloc(&c.kpairs, (size_t)(U * L.kp_ustride)));
+    KIVI_CUDA(dalloc(&c.vcodes, (size_t)(U * L.v_ustride)));
+    KIVI_CUDA(dalloc(&c.vpairs, (size_t)(U * L.vp_ustride)));
+    KIVI_CUDA(dalloc(&c.kring, (size_t)(U * L.ring_ustride)));
+    KIVI_CUDA(dalloc(&c.vring, (size_t)(U * L.ring_ustride)));
+    KIVI_CUDA(cudaMemsetAsync(c.kcodes, 0, (size_t)(U * L.k_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.vcodes, 0, (size_t)(U * L.v_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.kpairs, 0, sizeof(float2) * (size_t)(U * L.kp_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.vpairs, 0, sizeof(float2) * (size_t)(U * L.vp_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.kring, 0, sizeof(float) * (size_t)(U * L.ring_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.vring, 0, sizeof(float) * (size_t)(U * L.ring_ustride), st));
+    c.k_ustride = L.k_ustride;
+    c.kp_ustride = L.kp_ustride;
+    c.v_ustride = L.v_ustride;
+    c.vp_ustride = L.vp_ustride;
+    c.ring_ustride = L.ring_ustride;
+    h->cap = L.cap;
+    return KIVI_OK;
+}
+
+void init_dev_scalars(kivi_cache* h) {
+    h->dev.bits = h->cfg.bits;
+    h->dev.G = (int)h->cfg.group_size;
+    h->dev.R = (int)h->cfg.residual_length;
+    h->dev.d = (int)h->cfg.head_dim;
+    h->dev.maxc = (1 << h->cfg.bits) - 1;
+    h->dev.n_units = h->n_units;
+}
+
+uint64_t grouped_bytes(int64_t tokens, const kivi_config& cfg) {
+    // reference grouped_bytes (kv_cache.cpp:110-115): packed bytes + 4 B per group
+    const int64_t codes = tokens * cfg.head_dim;
+    return (uint64_t)ceil_div(codes * cfg.bits, 8) + 4ull * (uint64_t)(codes / cfg.group_size);
+}
+
+template <typename T>
+kivi_status ensure(T** p, int64_t* cap, int64_t need) {
+    if (need <= *cap) return KIVI_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    KIVI_CUDA(dalloc(p, (size_t)need));
+    *cap = need;
+    return KIVI_OK;
+}
+
+kivi_status ensure_capacity(kivi_cache* h, int64_t tokens, cudaStream_t st) {
+    if (tokens <= h->cap) return KIVI_OK;
+    return kivi_cache_reserve(h, std::max<int64_t>(tokens, 2 * h->cap), st);
+}
+
+bool fast_supported(const kivi_cache* h, int qpk) {
+    const kivi_config& c = h->cfg;
+    return qpk == 1 && c.head_dim == 128 && c.group_size == 32 && (c.bits == 2 || c.bits == 4);
+}
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <int B, int NSLOT>
+kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
+                        cudaStream_t st) {
+    using WS = fast::WarpSmem<NSLOT>;
+    const int64_t U = h->n_units;
+    const int64_t n_sub = ceil_div(h->l, fast::SUB);
+    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * fast::D);
+    if (rc) return rc;
+    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub);
+    if (rc) return rc;
+    rc = ensure(&h->stats, &h->stats_cap, U);
+    if (rc) return rc;
+
+    fast::FastArgs a;
+    a.c = h->dev;
+    a.l = h->l;
+    a.kg = h->kg();
+    a.vg = h->vg();
+    a.q = q;
+    a.qscale = qscale;
+    a.part_o = h->part_o;
+    a.part_ml = h->part_ml;
+    a.wlog = weights;
+    a.n_sub = n_sub;
+
+    const int smem_warp = (WS::BYTES + 127) & ~127;
+    const int smem = smem_warp * fast::WARPS;
+    if (h->fast_per_sm[B][NSLOT] == 0) {
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_fast_kernel<B, NSLOT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, fast::attend_fast_kernel<B, NSLOT>, fast::WARPS * 32, smem));
+        h->fast_per_sm[B][NSLOT] = per_sm < 1 ? 1 : per_sm;
+    }
+    const int per_sm = h->fast_per_sm[B][NSLOT];
+    const int64_t items = U * n_sub;
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
+                                           ceil_div(items, fast::WARPS));
+
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    fast::attend_fast_kernel<B, NSLOT><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
+    KIVI_LAUNCHED();
+    if (h->profile) {
+        cudaEventRecord(e1, st);
+        h->events.emplace_back(e0, e1);
+    }
+    h->main_launches++;
+    h->total_launches++;
+    fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, n_sub, out,
+                                                          weights ? h->stats : nullptr);
+    KIVI_LAUNCHED();
+    h->total_launches++;
+    if (weights) {
+        fast::normalize_weights_kernel<<<grid_for(U * h->l), 256, 0, st>>>(weights, h->stats, h->l,
+                                                                            U);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    return KIVI_OK;
+}
+
+kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, float* weights,
+                           int scale_logits, cudaStream_t st) {
+    const int64_t rows = h->n_units * qpk;
+    kivi_status rc = ensure(&h->scratch, &h->scratch_cap, rows * h->l);
+    if (rc) return rc;
+    AttendGenericArgs a;
+    a.c = h->dev;
+    a.l = h->l;
+    a.kg = h->kg();
+    a.vg = h->vg();
+    a.ring_mod = h->cfg.residual_length;
+    a.q = q;
+    a.qpk = qpk;
+    a.out = out;
+    a.weights = weights;
+    a.scratch = h->scratch;
+    a.scale_logits = scale_logits;
+    const size_t smem = sizeof(float) * (size_t)(h->cfg.head_dim + 32);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    attend_generic_kernel<<<(unsigned)rows, 256, smem, st>>>(a);
+    KIVI_LAUNCHED();
+    if (h->profile) {
+        cudaEventRecord(e1, st);
+        h->events.emplace_back(e0, e1);
+    }
+    h->main_launches++;
+    h->total_launches++;
+    return KIVI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kivi_last_error(void) { return g_last_error.c_str(); }
+int kivi_abi_version(void) { return KIVI_B200_ABI_VERSION; }
+kivi_status kivi_config_validate(const kivi_config* cfg) { return validate_cfg(cfg); }
+
+kivi_status kivi_cache_create(const kivi_config* cfg, int device, int64_t n_units,
+                              int64_t capacity_tokens, kivi_cache** out) {
+    if (!out) return fail(KIVI_ERR_USAGE, "out is NULL");
+    *out = nullptr;
+    kivi_status rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (n_units < 1) return fail(KIVI_ERR_USAGE, "n_units must be >= 1");
+    if (capacity_tokens < 0) return fail(KIVI_ERR_USAGE, "capacity_tokens must be >= 0");
+    DeviceGuard g(device);
+    kivi_cache* h = new kivi_cache();
+    h->cfg = *cfg;
+    h->device = device;
+    h->n_units = n_units;
+    init_dev_scalars(h);
+    rc = alloc_cache_buffers(h, make_layout(*cfg, capacity_tokens), nullptr);
+    if (rc) {
+        free_cache_buffers(h);
+        delete h;
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(nullptr);
+    if (e != cudaSuccess) {
+        free_cache_buffers(h);
+        delete h;
+        return fail(KIVI_ERR_CUDA, "create: %s", cudaGetErrorString(e));
+    }
+    *out = h;
+    return KIVI_OK;
+}
+
+kivi_status kivi_cache_destroy(kivi_cache* h) {
+    if (!h) return KIVI_OK;
+    DeviceGuard g(h->device);
+    cudaDeviceSynchronize();
+    free_cache_buffers(h);
+    cudaFree(h->part_o);
+    cudaFree(h->part_ml);
+    cudaFree(h->scratch);
+    cudaFree(h->stats);
+    cudaFree(h->st_q);
+    cudaFree(h->st_k);
+    cudaFree(h->st_v);
+    cudaFree(h->st_out);
+    cudaFree(h->st_w);
+    for (auto& ev : h->events) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    delete h;
+    return KIVI_OK;
+}
+
+kivi_status kivi_cache_reserve(kivi_cache* h, int64_t capacity_tokens, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    DeviceGuard g(h->device);
+    Layout L = make_layout(h->cfg, capacity_tokens);
+    if (L.cap <= h->cap) return KIVI_OK;
+    kivi_cache tmp;
+    tmp.cfg = h->cfg;
+    tmp.n_units = h->n_units;
+    cudaStream_t st = S(stream);
+    kivi_status rc = alloc_cache_buffers(&tmp, L, st);
+    if (rc) {
+        free_cache_buffers(&tmp);
+        return rc;
+    }
+    const CacheDev& o = h->dev;
+    CacheDev& n = tmp.dev;
+    const int64_t U = h->n_units;
+    KIVI_CUDA(cudaMemcpy2DAsync(n.kcodes, n.k_ustride, o.kcodes, o.k_ustride, o.k_ustride, U,
+                                cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpy2DAsync(n.kpairs, n.kp_ustride * sizeof(float2), o.kpairs,
+                                o.kp_ustride * sizeof(float2), o.kp_ustride * sizeof(float2), U,
+                                cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpy2DAsync(n.vcodes, n.v_ustride, o.vcodes, o.v_ustride, o.v_ustride, U,
+                                cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpy2DAsync(n.vpairs, n.vp_ustride * sizeof(float2), o.vpairs,
+                                o.vp_ustride * sizeof(float2), o.vp_ustride * sizeof(float2), U,
+                                cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.kring, o.kring, sizeof(float) * U * o.ring_ustride,
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.vring, o.vring, sizeof(float) * U * o.ring_ustride,
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaStreamSynchronize(st));
+    free_cache_buffers(h);
+    h->dev.kcodes = n.kcodes;
+    h->dev.kpairs = n.kpairs;
+    h->dev.vcodes = n.vcodes;
+    h->dev.vpairs = n.vpairs;
+    h->dev.kring = n.kring;
+    h->dev.vring = n.vring;
+    h->dev.k_ustride = n.k_ustride;
+    h->dev.kp_ustride = n.kp_ustride;
+    h->dev.v_ustride = n.v_ustride;
+    h->dev.vp_ustride = n.vp_ustride;
+    h->dev.ring_ustride = n.ring_ustride;
+    h->cap = tmp.cap;
+    return KIVI_OK;
+}
+
+kivi_status kivi_cache_clone(const kivi_cache* src, void* stream, kivi_cache** out) {
+    if (!src || !out) return fail(KIVI_ERR_USAGE, "NULL argument");
+    DeviceGuard g(src->device);
+    kivi_cache* h = nullptr;
+    kivi_status rc = kivi_cache_create(&src->cfg, src->device, src->n_units, src->cap, &h);
+    if (rc) return rc;
+    cudaStream_t st = S(stream);
+    const CacheDev& o = src->dev;
+    CacheDev& n = h->dev;
+    const int64_t U = src->n_units;
+    KIVI_CUDA(cudaMemcpyAsync(n.kcodes, o.kcodes, (size_t)(U * o.k_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.kpairs, o.kpairs, sizeof(float2) * (size_t)(U * o.kp_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.vcodes, o.vcodes, (size_t)(U * o.v_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.vpairs, o.vpairs, sizeof(float2) * (size_t)(U * o.vp_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.kring, o.kring, sizeof(float) * (size_t)(U * o.ring_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(n.vring, o.vring, sizeof(float) * (size_t)(U * o.ring_ustride),
+                              cudaMemcpyDeviceToDevice, st));
+    KIVI_CUDA(cudaStreamSynchronize(st));
+    h->l = src->l;
+    h->kres_cap = src->kres_cap;
+    h->vres_cap = src->vres_cap;
+    h->attend_path = src->attend_path;
+    *out = h;
+    return KIVI_OK;
+}
+
+kivi_status kivi_cache_get_info(const kivi_cache* h, kivi_cache_info* info) {
+    if (!h || !info) return fail(KIVI_ERR_USAGE, "NULL argument");
+    const int64_t R = h->cfg.residual_length, d = h->cfg.head_dim;
+    info->n_units = h->n_units;
+    info->capacity_tokens = h->cap;
+    info->total_tokens = h->l;
+    info->key_grouped_tokens = h->kg();
+    info->key_residual_rows = h->l - h->kg();
+    info->key_residual_capacity = h->kres_cap;
+    info->value_grouped_tokens = h->vg();
+    info->value_residual_rows = h->l - h->vg();
+    info->value_residual_capacity = h->vres_cap;
+    (void)R;
+    // reference memory_bytes (kv_cache.cpp:117-127): residual charged at its
+    // high-water capacity x residual.cols() (0 for a never-initialised state).
+    const uint64_t kcols = (h->l > 0 || h->kres_cap > 0) ? (uint64_t)d : 0;
+    info->key_memory_bytes = grouped_bytes(h->kg(), h->cfg) + 2ull * h->kres_cap * kcols;
+    info->value_memory_bytes = grouped_bytes(h->vg(), h->cfg) + 2ull * h->vres_cap * kcols;
+    const CacheDev& c = h->dev;
+    info->device_bytes = (uint64_t)h->n_units *
+                         ((uint64_t)c.k_ustride + (uint64_t)c.v_ustride +
+                          sizeof(float2) * (uint64_t)(c.kp_ustride + c.vp_ustride) +
+                          2 * sizeof(float) * (uint64_t)c.ring_ustride);
+    return KIVI_OK;
+}
+
+kivi_status kivi_prefill(kivi_cache* h, const float* keys, const float* values, int64_t l,
+                         void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (l <= 0) return fail(KIVI_ERR_USAGE, "prefill: empty prompt");
+    if (!keys || !values) return fail(KIVI_ERR_USAGE, "prefill: NULL keys/values");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    kivi_status rc = ensure_capacity(h, l, st);
+    if (rc) return rc;
+    CacheDev& c = h->dev;
+    const int64_t U = h->n_units;
+    // reset the code streams (appends OR into zeroed words)
+    KIVI_CUDA(cudaMemsetAsync(c.kcodes, 0, (size_t)(U * c.k_ustride), st));
+    KIVI_CUDA(cudaMemsetAsync(c.vcodes, 0, (size_t)(U * c.v_ustride), st));
+    const int64_t R = h->cfg.residual_length;
+    const int64_t kg = l - l % R;
+    const int64_t vg = l - std::min(l, R);
+    const int64_t G = h->cfg.group_size, d = h->cfg.head_dim;
+    if (kg > 0) {
+        prefill_keys_kernel<<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    if (vg > 0) {
+        prefill_values_kernel<<<grid_for(U * vg * (d / G)), 256, 0, st>>>(c, values, l, vg);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    prefill_residual_kernel<<<grid_for(U * (2 * l - kg - vg) * d), 256, 0, st>>>(c, keys, values,
+                                                                                 l, kg, vg);
+    KIVI_LAUNCHED();
+    h->total_launches++;
+    h->l = l;
+    h->kres_cap = l % R;  // kv_cache.cpp:40
+    h->vres_cap = std::min(l, R);
+    return KIVI_OK;
+}
+
+kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    kivi_status rc = ensure_capacity(h, h->l + 1, st);
+    if (rc) return rc;
+    append_kernel<<<(unsigned)h->n_units, 128, 0, st>>>(h->dev, t_k, t_v, h->l);
+    KIVI_LAUNCHED();
+    h->total_launches++;
+    const int64_t R = h->cfg.residual_length;
+    // residual_capacity = max(capacity, rows after the push) (kv_cache.cpp:78, 93-94)
+    const int64_t krows_after_push = h->l % R + 1;
+    h->kres_cap = std::max(h->kres_cap, krows_after_push);
+    const int64_t vrows = std::min(h->l, R) == R ? R : std::min(h->l, R) + 1;
+    h->vres_cap = std::max(h->vres_cap, vrows);
+    h->l += 1;
+    return KIVI_OK;
+}
+
+kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float* out,
+                        float* weights, int32_t scale_logits, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
+    if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "attend: NULL query/output");
+    if (h->l < 1) return fail(KIVI_ERR_USAGE, "attend: empty cache");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    const bool fast_ok = fast_supported(h, q_per_kv);
+    if (h->attend_path == 2 && !fast_ok)
+        return fail(KIVI_ERR_CONFIG, "fast attend path does not support this shape");
+    if (fast_ok && h->attend_path != 1) {
+        const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
+        const float qscale = scale * fast::LOG2E;
+        if (h->cfg.bits == 2) return launch_fast<2, 2>(h, t_q, out, weights, qscale, st);
+        return launch_fast<4, 2>(h, t_q, out, weights, qscale, st);
+    }
+    return launch_generic(h, t_q, q_per_kv, out, weights, scale_logits, st);
+}
+
+kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const float* t_v,
+                        int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
+                        void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
+    if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL query/output");
+    kivi_status rc = kivi_append(h, t_k, t_v, stream);
+    if (rc) return rc;
+    return kivi_attend(h, t_q, q_per_kv, out, weights, scale_logits, stream);
+}
+
+kivi_status kivi_prefill_host(kivi_cache* h, const float* keys, const float* values, int64_t l,
+                              void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (l <= 0) return fail(KIVI_ERR_USAGE, "prefill: empty prompt");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    const int64_t n = h->n_units * l * h->cfg.head_dim;
+    float *dk = nullptr, *dv = nullptr;
+    KIVI_CUDA(dalloc(&dk, (size_t)n));
+    KIVI_CUDA(dalloc(&dv, (size_t)n));
+    KIVI_CUDA(cudaMemcpyAsync(dk, keys, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(dv, values, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    kivi_status rc = kivi_prefill(h, dk, dv, l, stream);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(dk);
+    cudaFree(dv);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(KIVI_ERR_CUDA, "prefill_host: %s", cudaGetErrorString(e));
+    return KIVI_OK;
+}
+
+static kivi_status stage_rows(kivi_cache* h, int64_t qpk, int64_t wlen) {
+    const int64_t U = h->n_units, d = h->cfg.head_dim;
+    kivi_status rc;
+    if ((rc = ensure(&h->st_q, &h->st_cap_q, U * qpk * d))) return rc;
+    if ((rc = ensure(&h->st_out, &h->st_cap_out, U * qpk * d))) return rc;
+    if ((rc = ensure(&h->st_k, &h->st_cap_k, U * d))) return rc;
+    if ((rc = ensure(&h->st_v, &h->st_cap_v, U * d))) return rc;
+    if (wlen > 0 && (rc = ensure(&h->st_w, &h->st_cap_w, wlen))) return rc;
+    return KIVI_OK;
+}
+
+kivi_status kivi_append_host(kivi_cache* h, const float* t_k, const float* t_v, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
+    DeviceGuard g(h->device);
+    kivi_status rc = stage_rows(h, 1, 0);
+    if (rc) return rc;
+    cudaStream_t st = S(stream);
+    const size_t bytes = sizeof(float) * (size_t)(h->n_units * h->cfg.head_dim);
+    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, bytes, cudaMemcpyHostToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, bytes, cudaMemcpyHostToDevice, st));
+    return kivi_append(h, h->st_k, h->st_v, stream);
+}
+
+kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, const float* t_v,
+                             int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
+                             void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
+    if (!t_q || !t_k || !t_v || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL rows");
+    DeviceGuard g(h->device);
+    const int64_t U = h->n_units, d = h->cfg.head_dim;
+    const int64_t wlen = weights ? U * q_per_kv * (h->l + 1) : 0;
+    kivi_status rc = stage_rows(h, q_per_kv, wlen);
+    if (rc) return rc;
+    cudaStream_t st = S(stream);
+    KIVI_CUDA(cudaMemcpyAsync(h->st_q, t_q, sizeof(float) * U * q_per_kv * d,
+                              cudaMemcpyHostToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, sizeof(float) * U * d, cudaMemcpyHostToDevice, st));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, st));
+    rc = kivi_decode(h, h->st_q, h->st_k, h->st_v, q_per_kv, h->st_out, weights ? h->st_w : nullptr,
+                     scale_logits, stream);
+    if (rc) return rc;
+    KIVI_CUDA(cudaMemcpyAsync(out, h->st_out, sizeof(float) * U * q_per_kv * d,
+                              cudaMemcpyDeviceToHost, st));
+    if (weights)
+        KIVI_CUDA(cudaMemcpyAsync(weights, h->st_w, sizeof(float) * wlen, cudaMemcpyDeviceToHost, st));
+    return KIVI_OK;
+}
+
+kivi_status kivi_export_unit(const kivi_cache* h, int64_t unit, kivi_unit_state* dst,
+                             void* stream) {
+    if (!h || !dst) return fail(KIVI_ERR_USAGE, "NULL argument");
+    if (unit < 0 || unit >= h->n_units) return fail(KIVI_ERR_USAGE, "unit out of range");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    const CacheDev& c = h->dev;
+    const int64_t kg = h->kg(), vg = h->vg(), l = h->l;
+    const int64_t d = h->cfg.head_dim, G = h->cfg.group_size, B = h->cfg.bits;
+    const int64_t kgroups = kg * d / G, vgroups = vg * d / G;
+    const int64_t kr = l - kg, vr = l - vg;
+    double* tmp = nullptr;
+    const int64_t ntmp = 2 * (kgroups + vgroups) + (kr + vr) * d / 2 + 8;
+    KIVI_CUDA(dalloc(&tmp, (size_t)ntmp));
+    double *kz = tmp, *ks = kz + kgroups, *vz = ks + kgroups, *vs = vz + vgroups;
+    float* kres = reinterpret_cast<float*>(vs + vgroups);
+    float* vres = kres + kr * d;
+    if (kgroups)
+        pairs_to_zs_kernel<<<grid_for(kgroups), 256, 0, st>>>(c.kpairs + unit * c.kp_ustride,
+                                                               kgroups, c.maxc, kz, ks);
+    if (vgroups)
+        pairs_to_zs_kernel<<<grid_for(vgroups), 256, 0, st>>>(c.vpairs + unit * c.vp_ustride,
+                                                               vgroups, c.maxc, vz, vs);
+    if (kr)
+        KIVI_CUDA(cudaMemcpyAsync(kres, c.kring + unit * c.ring_ustride, sizeof(float) * kr * d,
+                                  cudaMemcpyDeviceToDevice, st));
+    if (vr)
+        ring_gather_kernel<<<grid_for(vr * d), 256, 0, st>>>(c.vring + unit * c.ring_ustride, vg, vr,
+                                                             c.R, c.d, vres);
+    KIVI_LAUNCHED();
+    const size_t kbytes = (size_t)ceil_div(kg * d * B, 8), vbytes = (size_t)ceil_div(vg * d * B, 8);
+    if (dst->key_packed && kbytes)
+        KIVI_CUDA(cudaMemcpyAsync(dst->key_packed, c.kcodes + unit * c.k_ustride, kbytes,
+                                  cudaMemcpyDeviceToHost, st));
+    if (dst->value_packed && vbytes)
+        KIVI_CUDA(cudaMemcpyAsync(dst->value_packed, c.vcodes + unit * c.v_ustride, vbytes,
+                                  cudaMemcpyDeviceToHost, st));
+    if (dst->key_zero && kgroups)
+        KIVI_CUDA(cudaMemcpyAsync(dst->key_zero, kz, 8 * kgroups, cudaMemcpyDeviceToHost, st));
+    if (dst->key_scale && kgroups)
+        KIVI_CUDA(cudaMemcpyAsync(dst->key_scale, ks, 8 * kgroups, cudaMemcpyDeviceToHost, st));
+    if (dst->value_zero && vgroups)
+        KIVI_CUDA(cudaMemcpyAsync(dst->value_zero, vz, 8 * vgroups, cudaMemcpyDeviceToHost, st));
+    if (dst->value_scale && vgroups)
+        KIVI_CUDA(cudaMemcpyAsync(dst->value_scale, vs, 8 * vgroups, cudaMemcpyDeviceToHost, st));
+    if (dst->key_residual && kr)
+        KIVI_CUDA(cudaMemcpyAsync(dst->key_residual, kres, sizeof(float) * kr * d,
+                                  cudaMemcpyDeviceToHost, st));
+    if (dst->value_residual && vr)
+        KIVI_CUDA(cudaMemcpyAsync(dst->value_residual, vres, sizeof(float) * vr * d,
+                                  cudaMemcpyDeviceToHost, st));
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(KIVI_ERR_CUDA, "export: %s", cudaGetErrorString(e));
+    return KIVI_OK;
+}
+
+kivi_status kivi_import_unit(kivi_cache* h, int64_t unit, int64_t total_tokens,
+                             int64_t key_residual_capacity, int64_t value_residual_capacity,
+                             const kivi_unit_state* src, void* stream) {
+    if (!h || !src) return fail(KIVI_ERR_USAGE, "NULL argument");
+    if (unit < 0 || unit >= h->n_units) return fail(KIVI_ERR_USAGE, "unit out of range");
+    if (total_tokens < 0) return fail(KIVI_ERR_USAGE, "negative token count");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    kivi_status rc = ensure_capacity(h, total_tokens, st);
+    if (rc) return rc;
+    h->l = total_tokens;
+    h->kres_cap = key_residual_capacity;
+    h->vres_cap = value_residual_capacity;
+    CacheDev& c = h->dev;
+    const int64_t kg = h->kg(), vg = h->vg(), l = h->l;
+    const int64_t d = h->cfg.head_dim, G = h->cfg.group_size, B = h->cfg.bits;
+    const int64_t kgroups = kg * d / G, vgroups = vg * d / G;
+    const int64_t kr = l - kg, vr = l - vg;
+    const size_t kbytes = (size_t)ceil_div(kg * d * B, 8), vbytes = (size_t)ceil_div(vg * d * B, 8);
+    if ((kgroups && (!src->key_packed || !src->key_zero || !src->key_scale)) ||
+        (vgroups && (!src->value_packed || !src->value_zero || !src->value_scale)) ||
+        (kr && !src->key_residual) || (vr && !src->value_residual))
+        return fail(KIVI_ERR_USAGE, "import: missing state buffers");
+    KIVI_CUDA(cudaMemsetAsync(c.kcodes + unit * c.k_ustride, 0, (size_t)c.k_ustride, st));
+    KIVI_CUDA(cudaMemsetAsync(c.vcodes + unit * c.v_ustride, 0, (size_t)c.v_ustride, st));
+    if (kbytes)
+        KIVI_CUDA(cudaMemcpyAsync(c.kcodes + unit * c.k_ustride, src->key_packed, kbytes,
+                                  cudaMemcpyHostToDevice, st));
+    if (vbytes)
+        KIVI_CUDA(cudaMemcpyAsync(c.vcodes + unit * c.v_ustride, src->value_packed, vbytes,
+                                  cudaMemcpyHostToDevice, st));
+    double* tmp = nullptr;
+    const int64_t ntmp = 2 * (kgroups + vgroups) + (kr + vr) * d / 2 + 8;
+    KIVI_CUDA(dalloc(&tmp, (size_t)ntmp));
+    double *kz = tmp, *ks = kz + kgroups, *vz = ks + kgroups, *vs = vz + vgroups;
+    float* kres = reinterpret_cast<float*>(vs + vgroups);
+    float* vres = kres + kr * d;
+    if (kgroups) {
+        KIVI_CUDA(cudaMemcpyAsync(kz, src->key_zero, 8 * kgroups, cudaMemcpyHostToDevice, st));
+        KIVI_CUDA(cudaMemcpyAsync(ks, src->key_scale, 8 * kgroups, cudaMemcpyHostToDevice, st));
+        zs_to_pairs_kernel<<<grid_for(kgroups), 256, 0, st>>>(kz, ks, kgroups, c.maxc,
+                                                               c.kpairs + unit * c.kp_ustride);
+    }
+    if (vgroups) {
+        KIVI_CUDA(cudaMemcpyAsync(vz, src->value_zero, 8 * vgroups, cudaMemcpyHostToDevice, st));
+        KIVI_CUDA(cudaMemcpyAsync(vs, src->value_scale, 8 * vgroups, cudaMemcpyHostToDevice, st));
+        zs_to_pairs_kernel<<<grid_for(vgroups), 256, 0, st>>>(vz, vs, vgroups, c.maxc,
+                                                               c.vpairs + unit * c.vp_ustride);
+    }
+    if (kr)
+        KIVI_CUDA(cudaMemcpyAsync(c.kring + unit * c.ring_ustride, src->key_residual,
+                                  sizeof(float) * kr * d, cudaMemcpyHostToDevice, st));
+    if (vr) {
+        KIVI_CUDA(cudaMemcpyAsync(vres, src->value_residual, sizeof(float) * vr * d,
+                                  cudaMemcpyHostToDevice, st));
+        ring_scatter_kernel<<<grid_for(vr * d), 256, 0, st>>>(c.vring + unit * c.ring_ustride, vg, vr,
+                                                              c.R, c.d, vres);
+    }
+    KIVI_LAUNCHED();
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(KIVI_ERR_CUDA, "import: %s", cudaGetErrorString(e));
+    return KIVI_OK;
+}
+
+kivi_status kivi_materialize(const kivi_cache* h, float* keys_out, float* values_out,
+                             void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    DeviceGuard g(h->device);
+    if (h->l == 0) return KIVI_OK;
+    cudaStream_t st = S(stream);
+    materialize_kernel<<<grid_for(h->n_units * h->l * h->cfg.head_dim), 256, 0, st>>>(
+        h->dev, h->l, h->kg(), h->vg(), keys_out, values_out);
+    KIVI_LAUNCHED();
+    return KIVI_OK;
+}
+
+kivi_status kivi_quantize_matrix(const float* m, int64_t rows, int64_t cols, int32_t bits,
+                                 int64_t group_size, kivi_axis axis, uint8_t* packed,
+                                 double* zero_points, double* scales, void* stream) {
+    if (bits < 1 || bits > 8) return fail(KIVI_ERR_CONFIG, "bits must be in [1, 8], got %d", bits);
+    if (group_size < 1) return fail(KIVI_ERR_CONFIG, "group_size must be >= 1");
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
+        return fail(KIVI_ERR_CONFIG,
+                    "packed storage requires bits in {1,2,4,8}; B=%d is fake-quant only", bits);
+    const int64_t extent = axis == KIVI_PER_CHANNEL ? rows : cols;
+    if (extent % group_size != 0)
+        return fail(KIVI_ERR_SHAPE,
+                    "quantize: %s grouped axis extent %lld not divisible by group size %lld "
+                    "(matrix %lldx%lld)",
+                    axis == KIVI_PER_CHANNEL ? "per_channel" : "per_token", (long long)extent,
+                    (long long)group_size, (long long)rows, (long long)cols);
+    if (rows * cols == 0) return KIVI_OK;
+    cudaStream_t st = S(stream);
+    const int64_t nbytes = ceil_div(rows * cols * bits, 8);
+    uint8_t* tmp = nullptr;
+    KIVI_CUDA(dalloc(&tmp, (size_t)round_up(nbytes, 4)));
+    KIVI_CUDA(cudaMemsetAsync(tmp, 0, (size_t)round_up(nbytes, 4), st));
+    quantize_matrix_kernel<<<grid_for(rows * cols / group_size), 256, 0, st>>>(
+        m, rows, cols, bits, (int)group_size, axis == KIVI_PER_CHANNEL, tmp, zero_points, scales);
+    cudaError_t le = cudaGetLastError();
+    cudaError_t ce = cudaMemcpyAsync(packed, tmp, (size_t)nbytes, cudaMemcpyDefault, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(le));
+    if (ce != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(ce));
+    if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(se));
+    return KIVI_OK;
+}
+
+kivi_status kivi_dequantize_matrix(const uint8_t* packed, const double* zero_points,
+                                   const double* scales, int64_t rows, int64_t cols, int32_t bits,
+                                   int64_t group_size, kivi_axis axis, float* out, void* stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
+        return fail(KIVI_ERR_USAGE, "unpack_codes: bits must be one of {1,2,4,8}");
+    if (group_size < 1) return fail(KIVI_ERR_CONFIG, "group_size must be >= 1");
+    if (rows * cols == 0) return KIVI_OK;
+    // read_code views the stream as 32-bit words: stage into a padded buffer.
+    cudaStream_t st = S(stream);
+    const int64_t nbytes = ceil_div(rows * cols * bits, 8);
+    uint8_t* tmp = nullptr;
+    KIVI_CUDA(dalloc(&tmp, (size_t)round_up(nbytes, 4)));
+    KIVI_CUDA(cudaMemsetAsync(tmp, 0, (size_t)round_up(nbytes, 4), st));
+    KIVI_CUDA(cudaMemcpyAsync(tmp, packed, (size_t)nbytes, cudaMemcpyDefault, st));
+    dequantize_matrix_kernel<<<grid_for(rows * cols), 256, 0, st>>>(
+        tmp, zero_points, scales, rows, cols, bits, (int)group_size, axis == KIVI_PER_CHANNEL, out);
+    cudaError_t le = cudaGetLastError();
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "dequantize: %s", cudaGetErrorString(le));
+    if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "dequantize: %s", cudaGetErrorString(se));
+    return KIVI_OK;
+}
+
+kivi_status kivi_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* bytes,
+                            void* stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
+        return fail(KIVI_ERR_USAGE, "pack_codes: bits must be one of {1,2,4,8}, got %d", bits);
+    if (n == 0) return KIVI_OK;
+    cudaStream_t st = S(stream);
+    int* bad = nullptr;
+    KIVI_CUDA(dalloc(&bad, 1));
+    KIVI_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    pack_codes_kernel<<<grid_for(ceil_div(n * bits, 8)), 256, 0, st>>>(codes, n, bits, bytes, bad);
+    int hbad = 0;
+    cudaError_t le = cudaGetLastError();
+    cudaError_t ce = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaFree(bad);
+    if (le != cudaSuccess || ce != cudaSuccess || se != cudaSuccess)
+        return fail(KIVI_ERR_CUDA, "pack_codes: %s",
+                    cudaGetErrorString(le != cudaSuccess ? le : (ce != cudaSuccess ? ce : se)));
+    if (hbad) return fail(KIVI_ERR_USAGE, "pack_codes: code exceeds 2^%d-1", bits);
+    return KIVI_OK;
+}
+
+kivi_status kivi_unpack_codes(const uint8_t* bytes, int64_t n, int32_t bits, uint8_t* codes,
+                              void* stream) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
+        return fail(KIVI_ERR_USAGE, "unpack_codes: bits must be one of {1,2,4,8}");
+    if (n == 0) return KIVI_OK;
+    unpack_codes_kernel<<<grid_for(n), 256, 0, S(stream)>>>(bytes, n, bits, codes);
+    KIVI_LAUNCHED();
+    return KIVI_OK;
+}
+
+kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* keys,
+                                     const float* values, int64_t l, int64_t d,
+                                     int32_t scale_logits, float* out, void* stream) {
+    if (n_q < 1 || d < 1) return fail(KIVI_ERR_SHAPE, "reference_attention: empty query");
+    if (l < 1) return fail(KIVI_ERR_SHAPE, "reference_attention: empty keys");
+    cudaStream_t st = S(stream);
+    float* scratch = nullptr;
+    KIVI_CUDA(dalloc(&scratch, (size_t)(n_q * l)));
+    AttendGenericArgs a{};
+    a.c.bits = 2;
+    a.c.G = 1;
+    a.c.R = (int)l;
+    a.c.d = (int)d;
+    a.c.maxc = 3;
+    a.c.n_units = 1;
+    a.c.kring = const_cast<float*>(keys);
+    a.c.vring = const_cast<float*>(values);
+    a.c.ring_ustride = 0;
+    a.l = l;
+    a.kg = 0;
+    a.vg = 0;
+    a.ring_mod = l;
+    a.q = q;
+    a.qpk = (int)n_q;
+    a.out = out;
+    a.weights = nullptr;
+    a.scratch = scratch;
+    a.scale_logits = scale_logits;
+    attend_generic_kernel<<<(unsigned)n_q, 256, sizeof(float) * (size_t)(d + 32), st>>>(a);
+    cudaError_t le = cudaGetLastError();
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaFree(scratch);
+    if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(le));
+    if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(se));
+    return KIVI_OK;
+}
+
+kivi_status kivi_set_attend_path(kivi_cache* h, int32_t path) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (path < 0 || path > 2) return fail(KIVI_ERR_USAGE, "path must be 0, 1 or 2");
+    h->attend_path = path;
+    return KIVI_OK;
+}
+
+kivi_status kivi_profile_enable(kivi_cache* h, int32_t enable) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    h->profile = enable != 0;
+    return KIVI_OK;
+}
+
+kivi_status kivi_profile_read(kivi_cache* h, double* main_kernel_ms, int64_t* main_launches,
+                              int64_t* total_launches) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    DeviceGuard g(h->device);
+    double ms = 0.0;
+    for (auto& ev : h->events) {
+        KIVI_CUDA(cudaEventSynchronize(ev.second));
+        float t = 0.f;
+        KIVI_CUDA(cudaEventElapsedTime(&t, ev.first, ev.second));
+        ms += t;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    h->events.clear();
+    if (main_kernel_ms) *main_kernel_ms = ms;
+    if (main_launches) *main_launches = h->main_launches;
+    if (total_launches) *total_launches = h->total_launches;
+    h->main_launches = 0;
+    h->total_launches = 0;
+    return KIVI_OK;
+}
+
+kivi_status kivi_attend_bytes(const kivi_cache* h, int32_t q_per_kv, uint64_t* bytes_per_unit) {
+    if (!h || !bytes_per_unit) return fail(KIVI_ERR_USAGE, "NULL argument");
+    // ceil(kg*d*B/8) + ceil(vg*d*B/8) + (kg*d/G + vg*d/G)*2*4
+    //             + (kr+vr)*d*4 + q_per_kv*d*4*2
+    const int64_t d = h->cfg.head_dim, G = h->cfg.group_size, B = h->cfg.bits;
+    const int64_t kg = h->kg(), vg = h->vg(), kr = h->l - kg, vr = h->l - vg;
+    *bytes_per_unit = (uint64_t)(ceil_div(kg * d * B, 8) + ceil_div(vg * d * B, 8) +
+                                 (kg * d / G + vg * d / G) * 8 + (kr + vr) * d * 4 +
+                                 (int64_t)q_per_kv * d * 8);
+    return KIVI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,364 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+The checker is the reference itself (oracle/_ref, compiled from its own
+sources) when present, else the plain-C port (oracle/liboracle.so).
+Bars:
+  * packed codes, zero-points, scales, residual rows, counters and
+    materialised K/V: bit-exact;
+  * decode outputs, generic kernel (reference arithmetic order): rel-L2 <= 1e-6;
+  * decode outputs, fast sm_100a kernel (fp32 FFMA2 accumulation):
+    rel-L2 <= 1e-5 (the reference's own hybrid bound, test_attention.cpp:79);
+  * softmax weights: max |diff| <= 1e-6 (generic), <= 1e-5 (fast).
+"""
+import numpy as np
+import pytest
+
+from oracles import Port, Ref, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+kb = pytest.importorskip("paper_2402_02750_b200")
+
+
+def checker():
+    return Ref() if Ref.available() else Port()
+
+
+def rnd(rng, *shape, scale=1.0):
+    return rng.uniform(-scale, scale, size=shape).astype(np.float32)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def assert_state_equal(got, want, where=""):
+    for k in ("key_packed", "key_zero", "key_scale", "key_residual", "value_packed",
+              "value_zero", "value_scale", "value_residual"):
+        g, w = np.asarray(got[k]), np.asarray(want[k])
+        assert g.shape == w.shape, f"{where} {k}: shape {g.shape} != {w.shape}"
+        assert g.tobytes() == w.tobytes(), f"{where} {k}: not bit-identical"
+
+
+def assert_counters(cache, unit_ref, where=""):
+    i = cache.info()
+    c = unit_ref.counters()
+    assert i["total_tokens"] == c["total"], where
+    assert i["key_grouped_tokens"] == c["key_grouped"], where
+    assert i["key_residual_rows"] == c["key_residual"], where
+    assert i["key_residual_capacity"] == c["key_capacity"], where
+    assert i["value_grouped_tokens"] == c["value_grouped"], where
+    assert i["value_residual_rows"] == c["value_residual"], where
+    assert i["value_residual_capacity"] == c["value_capacity"], where
+    assert i["key_memory_bytes"] == c["key_memory"], where
+    assert i["value_memory_bytes"] == c["value_memory"], where
+
+
+# (bits, G, R, d) — the reference tests' shapes plus the headline shape.
+STATE_CONFIGS = [
+    (2, 32, 128, 128), (4, 32, 128, 128), (8, 32, 128, 128), (1, 32, 64, 64),
+    (2, 4, 8, 8), (2, 8, 16, 32), (8, 4, 8, 4), (2, 2, 2, 2), (2, 2, 4, 2), (4, 2, 4, 2),
+    (2, 16, 32, 64), (1, 4, 8, 12), (4, 4, 8, 4), (2, 32, 512, 32),
+]
+
+
+# ---------------------------------------------------------------- quantizer --
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("G,per_channel", [(32, True), (32, False), (4, True), (2, False),
+                                           (3, True), (16, False)])
+def test_quantize_matrix_bit_exact(cuda, bits, G, per_channel):
+    ck = checker()
+    rng = np.random.default_rng(100 + bits * 7 + G)
+    rows, cols = (G * 6, 10) if per_channel else (9, G * 5)
+    m = rnd(rng, rows, cols, scale=3.0)
+    # degenerate / tie-heavy groups: constants, repeated values, +-0
+    m[:G, 0] = 1.25
+    m[:, 1] = np.round(m[:, 1] * 2) / 2
+    m[0, 2], m[1, 2] = 0.0, -0.0
+    p, z, s = kb.quantize_matrix(dev(m), bits, G, per_channel)
+    rp, rz, rs = ck.quantize_matrix(m, bits, G, per_channel)
+    assert p.cpu().numpy().tobytes() == rp.tobytes()
+    assert z.cpu().numpy().tobytes() == rz.tobytes()
+    assert s.cpu().numpy().tobytes() == rs.tobytes()
+    back = kb.dequantize_matrix(p, z, s, rows, cols, bits, G, per_channel).cpu().numpy()
+    want = np.zeros_like(m)
+    Port.lib().oracle_dequantize_matrix(rp.ctypes.data, rz.ctypes.data, rs.ctypes.data, rows,
+                                        cols, bits, G, int(per_channel), want.ctypes.data)
+    assert back.tobytes() == want.tobytes()
+
+
+def test_quantize_group_spec_examples(cuda):
+    # reference test_quantize.cpp:42-75 through the device quantizer
+    cases = [([0, 1, 2, 3], [0, 1, 2, 3], 0.0, 1.0), ([1, 1, 1], [0, 0, 0], 1.0, 1.0),
+             ([0.0, 0.1, 0.9, 1.0], [0, 0, 3, 3], 0.0, 1.0 / 3.0)]
+    for vals, codes, z0, s0 in cases:
+        m = np.array([vals], np.float32)
+        p, z, s = kb.quantize_matrix(dev(m), 2, len(vals), False)
+        got = kb.unpack_codes(p, len(vals), 2).cpu().numpy().tolist()
+        assert got == codes
+        assert z.cpu().item() == z0
+        assert abs(s.cpu().item() - s0) < 1e-15
+    # pack examples (test_quantize.cpp:100-108)
+    assert kb.pack_codes(dev(np.array([0, 1, 2, 3], np.uint8)), 2).cpu().tolist() == [0xE4]
+    assert kb.pack_codes(dev(np.array([3], np.uint8)), 2).cpu().tolist() == [0x03]
+    assert kb.pack_codes(dev(np.array([0xA, 0xB], np.uint8)), 4).cpu().tolist() == [0xBA]
+    with pytest.raises(kb.UsageError):
+        kb.pack_codes(dev(np.array([4], np.uint8)), 2)
+    with pytest.raises(kb.UsageError):
+        kb.pack_codes(dev(np.array([1], np.uint8)), 3)
+    with pytest.raises(kb.ShapeError):
+        kb.quantize_matrix(dev(rnd(np.random.default_rng(0), 5, 2)), 2, 2, True)
+    with pytest.raises(kb.ConfigError):
+        kb.quantize_matrix(dev(rnd(np.random.default_rng(0), 4, 2)), 3, 2, True)
+
+
+def test_pack_unpack_identity(cuda):
+    rng = np.random.default_rng(12)
+    for bits in (1, 2, 4, 8):
+        for n in (1, 7, 1000, 10001):
+            codes = rng.integers(0, 1 << bits, size=n, dtype=np.uint8)
+            p = kb.pack_codes(dev(codes), bits)
+            assert p.cpu().numpy().tobytes() == Port().pack_codes(codes, bits).tobytes()
+            assert kb.unpack_codes(p, n, bits).cpu().numpy().tobytes() == codes.tobytes()
+
+
+# ------------------------------------------------------------ cache state ----
+@pytest.mark.parametrize("cfg", STATE_CONFIGS)
+def test_prefill_then_stream_state_bit_exact(cuda, cfg):
+    bits, G, R, d = cfg
+    ck = checker()
+    rng = np.random.default_rng(hash(cfg) % 2**32)
+    U = 3
+    n = 3 * R + 7
+    K = rnd(rng, U, n, d)
+    V = rnd(rng, U, n, d)
+    K[1, :G, :] = 0.5  # constant key groups in unit 1
+    k0 = max(1, R // 2 + 3)
+    cache = kb.KVCache(kb.CacheConfig(bits, G, R, d), U)
+    cache.prefill(dev(K[:, :k0]), dev(V[:, :k0]))
+    refs = [ck.unit(bits, G, R, d) for _ in range(U)]
+    for u in range(U):
+        refs[u].prefill(K[u, :k0], V[u, :k0])
+    for t in range(k0, n + 1):
+        if t in (k0, k0 + 1, R, R + 1, 2 * R - 1, 2 * R, n):
+            torch.cuda.synchronize()
+            for u in range(U):
+                assert_state_equal(cache.export_unit(u), refs[u].export(), f"cfg={cfg} t={t} u={u}")
+                assert_counters(cache, refs[u], f"cfg={cfg} t={t}")
+            km, vm = cache.materialize()
+            for u in range(U):
+                rk, rv = refs[u].materialize()
+                assert km[u].cpu().numpy().tobytes() == rk.tobytes()
+                assert vm[u].cpu().numpy().tobytes() == rv.tobytes()
+        if t == n:
+            break
+        cache.append(dev(K[:, t]), dev(V[:, t]))
+        for u in range(U):
+            refs[u].append(K[u, t], V[u, t])
+
+
+def test_streaming_equals_batch(cuda):
+    # reference test_kv_cache.cpp:133-157 on the device path
+    rng = np.random.default_rng(25)
+    for trial in range(10):
+        bits, G, R, d = (2, 4, 8, 8)
+        n = int(rng.integers(1, 101))
+        k = int(rng.integers(1, n + 1))
+        K, V = rnd(rng, 1, n, d), rnd(rng, 1, n, d)
+        batch = kb.KVCache(kb.CacheConfig(bits, G, R, d), 1)
+        batch.prefill(dev(K), dev(V))
+        stream = kb.KVCache(kb.CacheConfig(bits, G, R, d), 1)
+        stream.prefill(dev(K[:, :k]), dev(V[:, :k]))
+        for t in range(k, n):
+            stream.append(dev(K[:, t]), dev(V[:, t]))
+        assert_state_equal(stream.export_unit(0), batch.export_unit(0), f"trial {trial}")
+
+
+# ----------------------------------------------------------------- decode ----
+def run_decode(cfg, U, l0, steps, path, seed, weights=True, scale=True):
+    bits, G, R, d = cfg
+    ck = checker()
+    rng = np.random.default_rng(seed)
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    cache = kb.KVCache(kb.CacheConfig(bits, G, R, d), U)
+    cache.set_attend_path(path)
+    cache.prefill(dev(K), dev(V))
+    refs = [ck.unit(bits, G, R, d) for _ in range(U)]
+    for u in range(U):
+        refs[u].prefill(K[u], V[u])
+    worst_out, worst_w = 0.0, 0.0
+    for s in range(steps):
+        q, tk, tv = rnd(rng, U, d), rnd(rng, U, d), rnd(rng, U, d)
+        res = cache.decode(dev(q)[:, None, :].contiguous(), dev(tk), dev(tv), weights=weights,
+                           scale_logits=scale)
+        out, w = res if weights else (res, None)
+        out = out.cpu().numpy()
+        w = w.cpu().numpy() if weights else None
+        for u in range(U):
+            ro, rw = refs[u].decode(q[u], tk[u], tv[u], scale_logits=scale, weights=True)
+            worst_out = max(worst_out, rel_l2(out[u, 0], ro))
+            if weights:
+                worst_w = max(worst_w, float(np.max(np.abs(w[u, 0] - rw))))
+    return worst_out, worst_w
+
+
+@pytest.mark.parametrize("cfg", [(2, 4, 8, 8), (2, 8, 16, 32), (4, 8, 16, 32), (8, 4, 8, 4),
+                                 (2, 32, 128, 128), (1, 16, 32, 64), (2, 2, 2, 2)])
+@pytest.mark.parametrize("l0", [1, 5, 17, 40])
+def test_decode_generic_vs_reference(cuda, cfg, l0):
+    e_out, e_w = run_decode(cfg, U=2, l0=l0 * cfg[2] // 8 + 1, steps=6, path="generic",
+                            seed=l0 * 31 + cfg[0])
+    assert e_out <= 1e-6, e_out
+    assert e_w <= 1e-6, e_w
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+@pytest.mark.parametrize("l0", [1, 31, 127, 128, 129, 255, 256, 257, 383, 600, 1153])
+def test_decode_fast_vs_reference(cuda, bits, l0):
+    cfg = (bits, 32, 128, 128)
+    e_out, e_w = run_decode(cfg, U=3, l0=l0, steps=4, path="fast", seed=l0 + bits)
+    assert e_out <= 1e-5, e_out
+    assert e_w <= 1e-5, e_w
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_decode_fast_across_flush_and_long_context(cuda, bits):
+    cfg = (bits, 32, 128, 128)
+    # 130 steps cross a key flush and 130 value pops; ctx ~4k like config 1.
+    e_out, _ = run_decode(cfg, U=2, l0=3968, steps=130, path="fast", seed=7, weights=False)
+    assert e_out <= 1e-5, e_out
+
+
+def test_fast_equals_generic_closely(cuda):
+    rng = np.random.default_rng(3)
+    U, d, l0 = 8, 128, 2000
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    a = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    a.prefill(dev(K), dev(V))
+    b = a.clone()
+    a.set_attend_path("fast")
+    b.set_attend_path("generic")
+    q = dev(rnd(rng, U, 1, d))
+    oa = a.attend(q).cpu().numpy()
+    ob = b.attend(q).cpu().numpy()
+    for u in range(U):
+        assert rel_l2(oa[u], ob[u]) <= 1e-5
+
+
+def test_gqa_generic_matches_per_head_reference(cuda):
+    # GQA: one append, q_per_kv query heads (reference emulates with copies)
+    ck = checker()
+    rng = np.random.default_rng(9)
+    cfg = (2, 32, 128, 128)
+    U, qpk, l0 = 2, 4, 300
+    K, V = rnd(rng, U, l0, 128), rnd(rng, U, l0, 128)
+    cache = kb.KVCache(kb.CacheConfig(*cfg), U)
+    cache.prefill(dev(K), dev(V))
+    q, tk, tv = rnd(rng, U, qpk, 128), rnd(rng, U, 128), rnd(rng, U, 128)
+    out = cache.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk).cpu().numpy()
+    for u in range(U):
+        for h in range(qpk):
+            r = ck.unit(*cfg)
+            r.prefill(K[u], V[u])
+            ro = r.decode(q[u, h], tk[u], tv[u])
+            assert rel_l2(out[u, h], ro) <= 1e-6
+
+
+def test_single_token_exact(cuda):
+    # reference test_attention.cpp:52-63
+    rng = np.random.default_rng(32)
+    cache = kb.KVCache(kb.CacheConfig(2, 4, 8, 4), 1)
+    q, tk, tv = rnd(rng, 1, 1, 4), rnd(rng, 1, 4), rnd(rng, 1, 4)
+    out, w = cache.decode(dev(q), dev(tk), dev(tv), weights=True)
+    assert out.cpu().numpy().reshape(-1).tobytes() == tv.reshape(-1).tobytes()
+    assert w.cpu().numpy().reshape(-1).tolist() == [1.0]
+
+
+def test_passthrough_bit_exact(cuda):
+    # reference test_attention.cpp:84-103: R >= l keeps everything fp32, and the
+    # decode equals reference_attention over the concatenated rows bitwise.
+    rng = np.random.default_rng(34)
+    for trial in range(10):
+        for d in (32, 64):
+            l = int(rng.integers(1, 301))
+            K, V = rnd(rng, 1, l, d), rnd(rng, 1, l, d)
+            cache = kb.KVCache(kb.CacheConfig(2, 32, 512, d), 1)
+            cache.prefill(dev(K), dev(V))
+            q, tk, tv = rnd(rng, 1, 1, d), rnd(rng, 1, d), rnd(rng, 1, d)
+            out = cache.decode(dev(q), dev(tk), dev(tv)).cpu().numpy().reshape(-1)
+            Kc = np.concatenate([K[0], tk], 0)
+            Vc = np.concatenate([V[0], tv], 0)
+            ref = kb.reference_attention(dev(q[0]), dev(Kc), dev(Vc)).cpu().numpy().reshape(-1)
+            assert out.tobytes() == ref.tobytes()
+
+
+def test_reference_attention_vs_reference(cuda):
+    ck = checker()
+    rng = np.random.default_rng(31)
+    for l, d, nq in ((1, 4, 1), (5, 3, 2), (300, 64, 3)):
+        q, K, V = rnd(rng, nq, d), rnd(rng, l, d), rnd(rng, l, d)
+        got = kb.reference_attention(dev(q), dev(K), dev(V)).cpu().numpy()
+        want = ck.reference_attention(q, K, V)
+        assert rel_l2(got, want) <= 1e-6
+
+
+def test_host_buffers_path_equals_device_path(cuda):
+    rng = np.random.default_rng(77)
+    U, d = 16, 128
+    K, V = rnd(rng, U, 700, d), rnd(rng, U, 700, d)
+    a = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    a.prefill_host(K, V)
+    b = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    b.prefill(dev(K), dev(V))
+    for _ in range(3):
+        q, tk, tv = rnd(rng, U, 1, d), rnd(rng, U, d), rnd(rng, U, d)
+        out_h = np.zeros((U, 1, d), np.float32)
+        a.decode_host(q, tk, tv, out_h)
+        torch.cuda.synchronize()
+        out_d = b.decode(dev(q), dev(tk), dev(tv)).cpu().numpy()
+        assert out_h.tobytes() == out_d.tobytes()
+
+
+def test_errors(cuda):
+    with pytest.raises(kb.ConfigError):
+        kb.KVCache(kb.CacheConfig(2, 32, 100, 64), 1)   # R % G != 0
+    with pytest.raises(kb.ConfigError):
+        kb.KVCache(kb.CacheConfig(2, 32, 128, 50), 1)   # d % G != 0
+    with pytest.raises(kb.ConfigError):
+        kb.KVCache(kb.CacheConfig(3, 2, 4, 2), 1)       # not packable
+    c = kb.KVCache(kb.CacheConfig(2, 2, 4, 2), 1)
+    with pytest.raises(kb.UsageError):
+        c.prefill(torch.zeros((1, 0, 2), device="cuda"), torch.zeros((1, 0, 2), device="cuda"))
+    with pytest.raises(kb.ShapeError):
+        c.append(torch.zeros((1, 3), device="cuda"), torch.zeros((1, 2), device="cuda"))
+
+
+def test_capacity_grows_on_append(cuda):
+    rng = np.random.default_rng(5)
+    c = kb.KVCache(kb.CacheConfig(2, 4, 8, 8), 2, capacity_tokens=8)
+    ck = checker()
+    refs = [ck.unit(2, 4, 8, 8) for _ in range(2)]
+    for t in range(50):
+        tk, tv = rnd(rng, 2, 8), rnd(rng, 2, 8)
+        c.append(dev(tk), dev(tv))
+        for u in range(2):
+            refs[u].append(tk[u], tv[u])
+    for u in range(2):
+        assert_state_equal(c.export_unit(u), refs[u].export())
+
+
+def test_import_export_roundtrip(cuda):
+    ck = checker()
+    rng = np.random.default_rng(8)
+    cfg = (2, 8, 16, 32)
+    r = ck.unit(*cfg)
+    r.prefill(rnd(rng, 77, 32), rnd(rng, 77, 32))
+    st = r.export()
+    cnt = r.counters()
+    c = kb.KVCache(kb.CacheConfig(*cfg), 1)
+    c.import_unit(0, int(cnt["total"]), int(cnt["key_capacity"]), int(cnt["value_capacity"]), st)
+    assert_state_equal(c.export_unit(0), st)
+    q, tk, tv = rnd(rng, 32), rnd(rng, 32), rnd(rng, 32)
+    out = c.decode(dev(q)[None, None], dev(tk)[None], dev(tv)[None]).cpu().numpy().reshape(-1)
+    assert rel_l2(out, r.decode(q, tk, tv)) <= 1e-6
