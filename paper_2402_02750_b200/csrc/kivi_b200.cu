@@ -250,6 +250,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                         cudaStream_t st) {
     using WS = fast::WarpSmem<NSLOT>;
     const int64_t U = h->n_units;
+    if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
+        return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * fast::D);
     if (rc) return rc;
@@ -260,18 +262,18 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
 
     fast::FastArgs a;
     a.c = h->dev;
-    a.l = h->l;
-    a.kg = h->kg();
-    a.vg = h->vg();
+    a.l = (int)h->l;
+    a.kg = (int)h->kg();
+    a.vg = (int)h->vg();
+    a.n_sub = (int)n_sub;
+    a.n_items = (int)(U * n_sub);
     a.q = q;
     a.qscale = qscale;
     a.part_o = h->part_o;
     a.part_ml = h->part_ml;
     a.wlog = weights;
-    a.n_sub = n_sub;
 
-    const int smem_warp = (WS::BYTES + 127) & ~127;
-    const int smem = smem_warp * fast::WARPS;
+    const int smem = WS::STRIDE * fast::WARPS;
     if (h->fast_per_sm[B][NSLOT] == 0) {
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_fast_kernel<B, NSLOT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -299,7 +301,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     }
     h->main_launches++;
     h->total_launches++;
-    fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, n_sub, out,
+    fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
                                                           weights ? h->stats : nullptr);
     KIVI_LAUNCHED();
     h->total_launches++;
