@@ -368,7 +368,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_spec_8TBs": achieved / 8000.0,
-                         "kernel": "kivi_b200::fast::attend_fast_kernel",
+                         "kernel": "kivi_b200::fast::attend_body_kernel + attend_tail_kernel",
                          "bytes_per_launch": per_launch_bytes, "avg_launch_us": avg_launch_s * 1e6,
                          "kernel_share_of_step": (kern_ms / 1e3) / elapsed},
             "cpu_baseline": cpu,

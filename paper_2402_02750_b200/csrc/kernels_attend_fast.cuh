@@ -103,8 +103,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
 struct FastArgs {
     CacheDev c;
     int l, kg, vg;
-    int n_sub;          // items per unit
-    int n_items;        // n_units * n_sub
+    int n_sub;          // partial slots per unit (= ceil(l / SUB))
+    int k_first;        // first sub-chunk index handled by this launch
+    int n_per_unit;     // sub-chunks per unit handled by this launch
+    int n_items;        // n_units * n_per_unit
     const float* q;     // [units][128]
     float qscale;       // logit scale * log2(e)
     float* part_o;      // [units][n_sub][128]
@@ -112,18 +114,415 @@ struct FastArgs {
     float* wlog;        // [units][l] log2-domain logits, or null
 };
 
+// Per-warp shared memory.  One q staging buffer suffices for NSLOT == 2: the
+// next item's first job is issued only after the current item's job 0 (which
+// consumes the staged q) has been computed, since every item has >= 2 jobs.
+template <int NSLOT>
+struct WarpSmem {
+    static_assert(NSLOT == 2, "q staging assumes two slots");
+    static constexpr int QRAW_OFF = NSLOT * SLOT;            // 128 fp32 (staged q)
+    static constexpr int QQ_OFF = QRAW_OFF + D * 4;          // 128 fp32 (q * scale * log2e)
+    static constexpr int PROBS_OFF = QQ_OFF + D * 4;         // 256 fp32
+    static constexpr int BAR_OFF = PROBS_OFF + SUB * 4;
+    static constexpr int BYTES = BAR_OFF + 8 * NSLOT;
+    static constexpr int STRIDE = (BYTES + 127) & ~127;
+};
+using WS2 = WarpSmem<2>;
+
+// ===================== shared compute bodies ===============================
+
+// q row (staged by TMA) -> q * scale * log2(e) table.
+__device__ __forceinline__ void load_q_table(const float* qraw, float* qq, float qscale, int lane) {
+    const float4 qv = reinterpret_cast<const float4*>(qraw)[lane];
+    reinterpret_cast<float4*>(qq)[lane] =
+        make_float4(qv.x * qscale, qv.y * qscale, qv.z * qscale, qv.w * qscale);
+    __syncwarp();
+}
+
+// Quantized key tiles -> logits.  The slot holds KQ_TILES tiles of codes
+// followed by KQ_TILES tiles of (lo, hi) pairs; lanes split as (tile, channel
+// slice); the 32 per-token partials are transpose-reduced through the slot.
+// Writes the logits of tiles [0, ntiles) to probs_dst[tile * 32 + token].
+template <int B>
+__device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* qq, float* probs_dst,
+                                                   int ntiles, float ksc, int lane) {
+    using PB = P<B>;
+    const int tl = lane / PB::LPT;  // tile within job
+    const int b = lane % PB::LPT;
+    float2 acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.f, 0.f);
+    float bias = 0.f;
+    if (tl < ntiles) {
+        const uint8_t* codes = slot + tl * PB::TILE_CODE;
+        const uint8_t* pairs = slot + PB::KQ_TILES * PB::TILE_CODE + tl * D * 8;
+        if constexpr (B == 2) {
+            // software-pipelined: the loads of iteration it+1 are issued
+            // before the 64 LOP3 + 32 FFMA2 of iteration it
+            uint4 cw = *reinterpret_cast<const uint4*>(codes + b * 16);
+            float4 pr = *reinterpret_cast<const float4*>(pairs + b * 16);
+            float2 qv = *reinterpret_cast<const float2*>(qq + 2 * b);
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                uint4 cw_n = cw;
+                float4 pr_n = pr;
+                float2 qv_n = qv;
+                if (it < 7) {
+                    const int ci = (it + 1) * PB::LPT + b;
+                    cw_n = *reinterpret_cast<const uint4*>(codes + ci * 16);
+                    pr_n = *reinterpret_cast<const float4*>(pairs + ci * 16);
+                    qv_n = *reinterpret_cast<const float2*>(qq + 2 * ci);
+                }
+                const float m0 = qv.x * ksc * (pr.y - pr.x);
+                const float m1 = qv.y * ksc * (pr.w - pr.z);
+                bias = fmaf(qv.x, pr.x, bias);
+                bias = fmaf(qv.y, pr.z, bias);
+                PB::fma_word(acc, cw.x, m0);
+                PB::fma_word(acc + 8, cw.y, m0);
+                PB::fma_word(acc, cw.z, m1);
+                PB::fma_word(acc + 8, cw.w, m1);
+                cw = cw_n;
+                pr = pr_n;
+                qv = qv_n;
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int ci = it * PB::LPT + b;
+                const uint4 cw = *reinterpret_cast<const uint4*>(codes + ci * 16);
+                const float2 pr = *reinterpret_cast<const float2*>(pairs + ci * 8);
+                const float qv = qq[ci];
+                const float m0 = qv * ksc * (pr.y - pr.x);
+                bias = fmaf(qv, pr.x, bias);
+                PB::fma_word(acc, cw.x, m0);
+                PB::fma_word(acc + 4, cw.y, m0);
+                PB::fma_word(acc + 8, cw.z, m0);
+                PB::fma_word(acc + 12, cw.w, m0);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < PB::LPT; o <<= 1) bias += __shfl_xor_sync(0xffffffffu, bias, o);
+    __syncwarp();
+    float* red = reinterpret_cast<float*>(slot);
+    {
+        float4* row = reinterpret_cast<float4*>(red + lane * 36);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            row[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
+    }
+    __syncwarp();
+    constexpr int TPL = 32 / PB::LPT;  // tokens per lane after the reduce
+    float sum[TPL];
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) sum[i] = 0.f;
+#pragma unroll
+    for (int bb = 0; bb < PB::LPT; ++bb) {
+        const float* src = red + (tl * PB::LPT + bb) * 36 + TPL * b;
+        if constexpr (TPL == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(src);
+            sum[0] += v.x; sum[1] += v.y; sum[2] += v.z; sum[3] += v.w;
+        } else {
+            const float2 v = *reinterpret_cast<const float2*>(src);
+            sum[0] += v.x; sum[1] += v.y;
+        }
+    }
+    if (tl < ntiles) {
+        float lg[TPL];
+#pragma unroll
+        for (int i = 0; i < TPL; ++i)
+            lg[i] = fmaf(sum[i], unscale_pos(PB::epos((TPL * b + i) % PB::TPW)), bias);
+        float* dst = probs_dst + tl * 32 + TPL * b;
+        if constexpr (TPL == 4)
+            *reinterpret_cast<float4*>(dst) = make_float4(lg[0], lg[1], lg[2], lg[3]);
+        else
+            *reinterpret_cast<float2*>(dst) = make_float2(lg[0], lg[1]);
+    }
+}
+
+// fp32 key residual rows -> logits.
+__device__ __forceinline__ void kf_rows_to_logits(const uint8_t* slot, const float* qq,
+                                                  float* probs_dst, int n, int lane) {
+    const float4 qa = reinterpret_cast<const float4*>(qq)[lane];
+    float mine = 0.f;
+    for (int r = 0; r < n; ++r) {
+        const float4 kv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
+        float v = qa.x * kv.x + qa.y * kv.y + qa.z * kv.z + qa.w * kv.w;
+        v = warp_sum(v);
+        if (lane == r) mine = v;
+    }
+    if (lane < n) probs_dst[lane] = mine;
+}
+
+// Softmax over the item's logits (in place, log2 domain); returns (max, sum).
+__device__ __forceinline__ float2 softmax_item(float* probs, int ntok, float* wlog_dst, int lane) {
+    __syncwarp();
+    float mx = -INFINITY;
+    for (int i = lane; i < ntok; i += 32) mx = fmaxf(mx, probs[i]);
+    mx = warp_max(mx);
+    float sm = 0.f;
+    for (int i = lane; i < ntok; i += 32) {
+        const float lg = probs[i];
+        if (wlog_dst) wlog_dst[i] = lg;
+        const float e = ex2_approx(lg - mx);
+        probs[i] = e;
+        sm += e;
+    }
+    sm = warp_sum(sm);
+    __syncwarp();
+    return make_float2(mx, sm);
+}
+
+// Quantized value tokens -> P.V accumulators.  Lane = (jj, h): token offset
+// jj in 0..15, channel half h (channels 64h .. 64h+63 = groups 2h, 2h+1).
+template <int B>
+__device__ __forceinline__ void vq_tokens_accumulate(const uint8_t* slot, const float* pr_tok, int n,
+                                                     float ksc, float2* vacc, float& zacc0,
+                                                     float& zacc1, int lane) {
+    using PB = P<B>;
+    const int h = lane & 1, jj = lane >> 1;
+    const uint8_t* pairs = slot + PB::VQ_TOK * PB::TOK_CODE;
+    if constexpr (B == 2) {
+        int t = jj;
+        uint4 cw = make_uint4(0, 0, 0, 0);
+        float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
+        float pt = 0.f;
+        if (t < n) {
+            cw = *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 16);
+            pr = *reinterpret_cast<const float4*>(pairs + t * 32 + h * 16);
+            pt = pr_tok[t];
+        }
+        for (; t < n; t += 16) {
+            const int tn = t + 16;  // prefetch the next token of this lane
+            uint4 cw_n = cw;
+            float4 pr_n = pr;
+            float pt_n = pt;
+            if (tn < n) {
+                cw_n = *reinterpret_cast<const uint4*>(slot + tn * PB::TOK_CODE + h * 16);
+                pr_n = *reinterpret_cast<const float4*>(pairs + tn * 32 + h * 16);
+                pt_n = pr_tok[tn];
+            }
+            const float pk = pt * ksc;
+            const float ws0 = pk * (pr.y - pr.x);
+            const float ws1 = pk * (pr.w - pr.z);
+            zacc0 = fmaf(pt, pr.x, zacc0);
+            zacc1 = fmaf(pt, pr.z, zacc1);
+            PB::fma_word(vacc, cw.x, ws0);
+            PB::fma_word(vacc + 8, cw.y, ws0);
+            PB::fma_word(vacc + 16, cw.z, ws1);
+            PB::fma_word(vacc + 24, cw.w, ws1);
+            cw = cw_n;
+            pr = pr_n;
+            pt = pt_n;
+        }
+    } else {
+        for (int t = jj; t < n; t += 16) {
+            const float pt = pr_tok[t];
+            const float4 pr = *reinterpret_cast<const float4*>(pairs + t * 32 + h * 16);
+            const float pk = pt * ksc;
+            const float ws0 = pk * (pr.y - pr.x);
+            const float ws1 = pk * (pr.w - pr.z);
+            zacc0 = fmaf(pt, pr.x, zacc0);
+            zacc1 = fmaf(pt, pr.z, zacc1);
+            const uint4 c0 = *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 32);
+            const uint4 c1 = *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 32 + 16);
+            PB::fma_word(vacc, c0.x, ws0);
+            PB::fma_word(vacc + 4, c0.y, ws0);
+            PB::fma_word(vacc + 8, c0.z, ws0);
+            PB::fma_word(vacc + 12, c0.w, ws0);
+            PB::fma_word(vacc + 16, c1.x, ws1);
+            PB::fma_word(vacc + 20, c1.y, ws1);
+            PB::fma_word(vacc + 24, c1.z, ws1);
+            PB::fma_word(vacc + 28, c1.w, ws1);
+        }
+    }
+}
+
+// fp32 value residual rows -> P.V (lane owns channels 4*lane .. 4*lane+3).
+__device__ __forceinline__ void vf_rows_accumulate(const uint8_t* slot, const float* pr_tok, int n,
+                                                   float4& facc, int lane) {
+    for (int r = 0; r < n; ++r) {
+        const float4 vv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
+        const float pt = pr_tok[r];
+        facc.x = fmaf(pt, vv.x, facc.x);
+        facc.y = fmaf(pt, vv.y, facc.y);
+        facc.z = fmaf(pt, vv.z, facc.z);
+        facc.w = fmaf(pt, vv.w, facc.w);
+    }
+}
+
+// Reduce the value accumulators across the 16 lanes sharing a channel half
+// (32 rows x 64 channels through the slot, 16-byte chunks XOR-swizzled by
+// row: conflict-free writes and reads) and write the item's partial.
+template <int B>
+__device__ __forceinline__ void v_finalize(uint8_t* slot, const float2* vacc, float zacc0,
+                                           float zacc1, const float4& facc, float2 ml,
+                                           float* part_o, float2* part_ml, int lane) {
+    using PB = P<B>;
+    __syncwarp();
+    float4* red = reinterpret_cast<float4*>(slot);
+#pragma unroll
+    for (int qc = 0; qc < 16; ++qc)
+        red[lane * 16 + (qc ^ (lane & 7))] =
+            make_float4(vacc[2 * qc].x, vacc[2 * qc].y, vacc[2 * qc + 1].x, vacc[2 * qc + 1].y);
+    float z0 = zacc0, z1 = zacc1;
+#pragma unroll
+    for (int o = 2; o < 32; o <<= 1) {
+        z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+        z1 += __shfl_xor_sync(0xffffffffu, z1, o);
+    }
+    __syncwarp();
+    const int ho = lane >> 4;  // output channel half of this lane
+    const int qc = lane & 15;  // 16-byte chunk within the half
+    const float zh0 = __shfl_sync(0xffffffffu, z0, ho);
+    const float zh1 = __shfl_sync(0xffffffffu, z1, ho);
+    const float z = ((lane >> 3) & 1) ? zh1 : zh0;
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r2 = 0; r2 < 16; ++r2) {
+        const int row = r2 * 2 + ho;
+        const float4 v = red[row * 16 + (qc ^ (row & 7))];
+        s4.x += v.x; s4.y += v.y; s4.z += v.z; s4.w += v.w;
+    }
+    const int m0 = (4 * qc) & 31;  // channel within its 32-channel group
+    float4 o;
+    o.x = fmaf(s4.x, unscale_pos(PB::epos((m0 + 0) % PB::TPW)), z) + facc.x;
+    o.y = fmaf(s4.y, unscale_pos(PB::epos((m0 + 1) % PB::TPW)), z) + facc.y;
+    o.z = fmaf(s4.z, unscale_pos(PB::epos((m0 + 2) % PB::TPW)), z) + facc.z;
+    o.w = fmaf(s4.w, unscale_pos(PB::epos((m0 + 3) % PB::TPW)), z) + facc.w;
+    reinterpret_cast<float4*>(part_o)[lane] = o;
+    if (lane == 0) *part_ml = ml;
+}
+
+// ===================== K4a: body kernel (fully quantized items) =============
+// Items are whole 256-token sub-chunks below floor32(vg): every token's key
+// and value are quantized, so the job sequence is fixed (B=2: 2 key jobs of 4
+// tiles, 2 value jobs of 128 tokens) and the issue path is straight-line.
+template <int B>
+__global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) {
+    using PB = P<B>;
+    constexpr int NKJ = (SUB / 32) / PB::KQ_TILES;  // key jobs per item
+    constexpr int NVJ = SUB / PB::VQ_TOK;           // value jobs per item
+    constexpr int NJ = NKJ + NVJ;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* wbase = smem_raw + warp * WS2::STRIDE;
+    float* qraw = reinterpret_cast<float*>(wbase + WS2::QRAW_OFF);
+    float* qq = reinterpret_cast<float*>(wbase + WS2::QQ_OFF);
+    float* probs = reinterpret_cast<float*>(wbase + WS2::PROBS_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WS2::BAR_OFF);
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint64_t policy = make_evict_first_policy();
+    const CacheDev& c = a.c;
+    const int gw = blockIdx.x * WARPS + warp;
+    const int tw = gridDim.x * WARPS;
+    const int nper = a.n_per_unit;
+    const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
+
+    int f_item = gw, f_job = 0;
+    int f_u = f_item / nper, f_k = f_item - f_u * nper;
+    auto issue_next = [&](int s) {
+        if (f_item >= a.n_items) return;
+        if (lane == 0) {
+            uint8_t* slot = wbase + s * SLOT;
+            uint64_t* bar = &bars[s];
+            fence_proxy_async_smem();
+            if (f_job < NKJ) {
+                const int64_t tile0 = (int64_t)f_k * (SUB / 32) + f_job * PB::KQ_TILES;
+                constexpr uint32_t cb = PB::KQ_TILES * PB::TILE_CODE;
+                constexpr uint32_t pb = PB::KQ_TILES * D * 8;
+                mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? D * 4 : 0));
+                bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE, cb,
+                                     bar, policy);
+                bulk_g2s_evict_first(slot + cb, c.kpairs + f_u * c.kp_ustride + tile0 * D, pb, bar,
+                                     policy);
+                if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * D, D * 4, bar);
+            } else {
+                const int64_t ts = (int64_t)f_k * SUB + (f_job - NKJ) * PB::VQ_TOK;
+                constexpr uint32_t cb = PB::VQ_TOK * PB::TOK_CODE;
+                constexpr uint32_t pb = PB::VQ_TOK * (D / G) * 8;
+                mbar_arrive_expect_tx(bar, cb + pb);
+                bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb, bar,
+                                     policy);
+                bulk_g2s_evict_first(slot + cb, c.vpairs + f_u * c.vp_ustride + ts * (D / G), pb, bar,
+                                     policy);
+            }
+        }
+        if (++f_job == NJ) {
+            f_job = 0;
+            f_item += tw;
+            f_u = f_item / nper;
+            f_k = f_item - f_u * nper;
+        }
+    };
+    issue_next(0);
+    issue_next(1);
+
+    uint32_t phase = 0;
+    int cs = 0;
+    auto wait_slot = [&]() -> uint8_t* {
+        mbar_wait(&bars[cs], (phase >> cs) & 1u);
+        phase ^= (1u << cs);
+        return wbase + cs * SLOT;
+    };
+    auto release_slot = [&]() {
+        __syncwarp();
+        issue_next(cs);
+        cs ^= 1;
+    };
+
+    for (int item = gw; item < a.n_items; item += tw) {
+        const int u = item / nper;
+        const int k = a.k_first + (item - u * nper);
+#pragma unroll 1
+        for (int jk = 0; jk < NKJ; ++jk) {
+            uint8_t* slot = wait_slot();
+            if (jk == 0) load_q_table(qraw, qq, a.qscale, lane);
+            kq_tiles_to_logits<B>(slot, qq, probs + jk * PB::KQ_TILES * 32, PB::KQ_TILES, ksc,
+                                  lane);
+            release_slot();
+        }
+        const float2 ml = softmax_item(
+            probs, SUB, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * SUB : nullptr, lane);
+        float2 vacc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) vacc[i] = make_float2(0.f, 0.f);
+        float zacc0 = 0.f, zacc1 = 0.f;
+#pragma unroll 1
+        for (int jv = 0; jv < NVJ; ++jv) {
+            uint8_t* slot = wait_slot();
+            vq_tokens_accumulate<B>(slot, probs + jv * PB::VQ_TOK, PB::VQ_TOK, ksc, vacc, zacc0,
+                                    zacc1, lane);
+            if (jv == NVJ - 1) {
+                const int64_t pi = (int64_t)u * a.n_sub + k;
+                v_finalize<B>(slot, vacc, zacc0, zacc1, make_float4(0.f, 0.f, 0.f, 0.f), ml,
+                              a.part_o + pi * D, a.part_ml + pi, lane);
+            }
+            release_slot();
+        }
+    }
+}
+
+// ===================== K4b: tail kernel (items with residual tokens) ========
+
 enum JobKind { KQ = 0, KF = 1, VQ = 2, VF = 3 };
 
 struct ItemPlan {
-    int u, t0, t1;
+    int u, k, t0, t1;
     int nkq, nkf, nvq, nvf, njobs;
 };
 
 template <int B>
 __device__ __forceinline__ ItemPlan plan_item(const FastArgs& a, int item) {
     ItemPlan p;
-    p.u = item / a.n_sub;
-    p.t0 = (item - p.u * a.n_sub) * SUB;
+    p.u = item / a.n_per_unit;
+    p.k = a.k_first + (item - p.u * a.n_per_unit);
+    p.t0 = p.k * SUB;
     p.t1 = min(p.t0 + SUB, a.l);
     const int kq = max(0, min(p.t1, a.kg) - p.t0);
     const int kf = p.t1 - max(p.t0, a.kg);
@@ -220,44 +619,29 @@ __device__ __forceinline__ void issue_job(const FastArgs& a, int u, const JobDes
     if (with_q) bulk_g2s(qraw, a.q + (int64_t)u * D, qb, bar);
 }
 
-// Per-warp shared memory.  One q staging buffer suffices for NSLOT == 2: the
-// next item's first job is issued only after the current item's job 0 (which
-// consumes the staged q) has been computed, since every item has >= 2 jobs.
-template <int NSLOT>
-struct WarpSmem {
-    static_assert(NSLOT == 2, "q staging assumes two slots");
-    static constexpr int QRAW_OFF = NSLOT * SLOT;            // 128 fp32 (staged q)
-    static constexpr int QQ_OFF = QRAW_OFF + D * 4;          // 128 fp32 (q * scale * log2e)
-    static constexpr int PROBS_OFF = QQ_OFF + D * 4;         // 256 fp32
-    static constexpr int BAR_OFF = PROBS_OFF + SUB * 4;
-    static constexpr int BYTES = BAR_OFF + 8 * NSLOT;
-    static constexpr int STRIDE = (BYTES + 127) & ~127;
-};
-
-template <int B, int NSLOT>
-__global__ void __launch_bounds__(WARPS * 32, 3) attend_fast_kernel(FastArgs a) {
+// Any mix of quantized / fp32 keys and values per item (the residual window
+// and the last partial sub-chunk), any l.
+template <int B>
+__global__ void __launch_bounds__(WARPS * 32, 3) attend_tail_kernel(FastArgs a) {
     using PB = P<B>;
-    using WS = WarpSmem<NSLOT>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* wbase = smem_raw + warp * WS::STRIDE;
-    float* qraw = reinterpret_cast<float*>(wbase + WS::QRAW_OFF);
-    float* qq = reinterpret_cast<float*>(wbase + WS::QQ_OFF);
-    float* probs = reinterpret_cast<float*>(wbase + WS::PROBS_OFF);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WS::BAR_OFF);
-
+    uint8_t* wbase = smem_raw + warp * WS2::STRIDE;
+    float* qraw = reinterpret_cast<float*>(wbase + WS2::QRAW_OFF);
+    float* qq = reinterpret_cast<float*>(wbase + WS2::QQ_OFF);
+    float* probs = reinterpret_cast<float*>(wbase + WS2::PROBS_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WS2::BAR_OFF);
     if (lane == 0) {
-        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[s], 1);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
     __syncwarp();
     const uint64_t policy = make_evict_first_policy();
-
     const int gw = blockIdx.x * WARPS + warp;
     const int tw = gridDim.x * WARPS;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
 
-    // ---- fetch cursor (uniform across the warp) ----------------------------
     int f_item = gw, f_job = 0;
     ItemPlan f_plan{};
     if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
@@ -274,177 +658,37 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_fast_kernel(FastArgs a) 
             if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
         }
     };
-#pragma unroll
-    for (int s = 0; s < NSLOT; ++s) issue_next(s);
+    issue_next(0);
+    issue_next(1);
 
     uint32_t phase = 0;
-    int cs = 0;  // compute slot
-
+    int cs = 0;
     auto wait_slot = [&]() -> uint8_t* {
         mbar_wait(&bars[cs], (phase >> cs) & 1u);
         phase ^= (1u << cs);
         return wbase + cs * SLOT;
     };
-    auto release_slot = [&](bool) {
+    auto release_slot = [&]() {
         __syncwarp();
         issue_next(cs);
-        cs = (cs + 1 == NSLOT) ? 0 : cs + 1;
+        cs ^= 1;
     };
 
     for (int item = gw; item < a.n_items; item += tw) {
         const ItemPlan p = plan_item<B>(a, item);
-        const int u = p.u;
-        const int ntok = p.t1 - p.t0;
         const int nk = p.nkq + p.nkf;
-
-        // ================= phase 1: logits of the item's tokens =============
         for (int j = 0; j < nk; ++j) {
             uint8_t* slot = wait_slot();
-            if (j == 0) {
-                // query row arrived with the item's first job
-                const float4 qv = reinterpret_cast<const float4*>(qraw)[lane];
-                reinterpret_cast<float4*>(qq)[lane] = make_float4(
-                    qv.x * a.qscale, qv.y * a.qscale, qv.z * a.qscale, qv.w * a.qscale);
-                __syncwarp();
-            }
+            if (j == 0) load_q_table(qraw, qq, a.qscale, lane);
             const JobDesc jd = job_of<B>(a, p, j);
-            if (jd.kind == KQ) {
-                const int tl = lane / PB::LPT;  // tile within job
-                const int b = lane % PB::LPT;
-                float2 acc[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.f, 0.f);
-                float bias = 0.f;
-                if (tl < jd.n) {
-                    const uint8_t* codes = slot + tl * PB::TILE_CODE;
-                    const uint8_t* pairs = slot + PB::KQ_TILES * PB::TILE_CODE + tl * D * 8;
-                    if constexpr (B == 2) {
-                        // software-pipelined: loads of iteration it+1 issued before
-                        // the 64 LOP3 + 32 FFMA2 of iteration it
-                        uint4 cw = *reinterpret_cast<const uint4*>(codes + b * 16);
-                        float4 pr = *reinterpret_cast<const float4*>(pairs + b * 16);
-                        float2 qv = *reinterpret_cast<const float2*>(qq + 2 * b);
-#pragma unroll
-                        for (int it = 0; it < 8; ++it) {
-                            uint4 cw_n = cw;
-                            float4 pr_n = pr;
-                            float2 qv_n = qv;
-                            if (it < 7) {
-                                const int ci = (it + 1) * PB::LPT + b;
-                                cw_n = *reinterpret_cast<const uint4*>(codes + ci * 16);
-                                pr_n = *reinterpret_cast<const float4*>(pairs + ci * 16);
-                                qv_n = *reinterpret_cast<const float2*>(qq + 2 * ci);
-                            }
-                            const float m0 = qv.x * ksc * (pr.y - pr.x);
-                            const float m1 = qv.y * ksc * (pr.w - pr.z);
-                            bias = fmaf(qv.x, pr.x, bias);
-                            bias = fmaf(qv.y, pr.z, bias);
-                            PB::fma_word(acc, cw.x, m0);
-                            PB::fma_word(acc + 8, cw.y, m0);
-                            PB::fma_word(acc, cw.z, m1);
-                            PB::fma_word(acc + 8, cw.w, m1);
-                            cw = cw_n;
-                            pr = pr_n;
-                            qv = qv_n;
-                        }
-                    } else {
-#pragma unroll
-                        for (int it = 0; it < 8; ++it) {
-                            const int ci = it * PB::LPT + b;
-                            const uint4 cw = *reinterpret_cast<const uint4*>(codes + ci * 16);
-                            const float2 pr = *reinterpret_cast<const float2*>(pairs + ci * 8);
-                            const float qv = qq[ci];
-                            const float m0 = qv * ksc * (pr.y - pr.x);
-                            bias = fmaf(qv, pr.x, bias);
-                            PB::fma_word(acc, cw.x, m0);
-                            PB::fma_word(acc + 4, cw.y, m0);
-                            PB::fma_word(acc + 8, cw.z, m0);
-                            PB::fma_word(acc + 12, cw.w, m0);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int o = 1; o < PB::LPT; o <<= 1) bias += __shfl_xor_sync(0xffffffffu, bias, o);
-                // transpose-reduce the 32 per-token partials through the slot
-                __syncwarp();
-                float* red = reinterpret_cast<float*>(slot);
-                {
-                    float4* row = reinterpret_cast<float4*>(red + lane * 36);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        row[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x,
-                                             acc[2 * i + 1].y);
-                }
-                __syncwarp();
-                constexpr int TPL = 32 / PB::LPT;  // tokens per lane after the reduce
-                float sum[TPL];
-#pragma unroll
-                for (int i = 0; i < TPL; ++i) sum[i] = 0.f;
-#pragma unroll
-                for (int bb = 0; bb < PB::LPT; ++bb) {
-                    const float* src = red + (tl * PB::LPT + bb) * 36 + TPL * b;
-                    if constexpr (TPL == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(src);
-                        sum[0] += v.x; sum[1] += v.y; sum[2] += v.z; sum[3] += v.w;
-                    } else {
-                        const float2 v = *reinterpret_cast<const float2*>(src);
-                        sum[0] += v.x; sum[1] += v.y;
-                    }
-                }
-                if (tl < jd.n) {
-                    const int tok_in_item = (jd.ts - p.t0) + tl * 32;
-                    float lg[TPL];
-#pragma unroll
-                    for (int i = 0; i < TPL; ++i) {
-                        const int tok = TPL * b + i;  // token within tile
-                        lg[i] = fmaf(sum[i], unscale_pos(PB::epos(tok % PB::TPW)), bias);
-                    }
-                    if constexpr (TPL == 4)
-                        *reinterpret_cast<float4*>(probs + tok_in_item + TPL * b) =
-                            make_float4(lg[0], lg[1], lg[2], lg[3]);
-                    else
-                        *reinterpret_cast<float2*>(probs + tok_in_item + TPL * b) =
-                            make_float2(lg[0], lg[1]);
-                }
-            } else {
-                // ---- fp32 key residual rows -> logits -----------------------
-                const float4 qa = reinterpret_cast<const float4*>(qq)[lane];
-                float mine = 0.f;
-                for (int r = 0; r < jd.n; ++r) {
-                    const float4 kv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
-                    float v = qa.x * kv.x + qa.y * kv.y + qa.z * kv.z + qa.w * kv.w;
-                    v = warp_sum(v);
-                    if (lane == r) mine = v;
-                }
-                if (lane < jd.n) probs[jd.ts - p.t0 + lane] = mine;
-            }
-            release_slot(jd.kind == KQ);
+            if (jd.kind == KQ)
+                kq_tiles_to_logits<B>(slot, qq, probs + (jd.ts - p.t0), jd.n, ksc, lane);
+            else
+                kf_rows_to_logits(slot, qq, probs + (jd.ts - p.t0), jd.n, lane);
+            release_slot();
         }
-
-        // ================= softmax over the item (log2 domain) ===============
-        __syncwarp();
-        float m_item, l_item;
-        {
-            float mx = -INFINITY;
-            for (int i = lane; i < ntok; i += 32) mx = fmaxf(mx, probs[i]);
-            mx = warp_max(mx);
-            float sm = 0.f;
-            for (int i = lane; i < ntok; i += 32) {
-                const float lg = probs[i];
-                if (a.wlog) a.wlog[(int64_t)u * a.l + p.t0 + i] = lg;
-                const float e = ex2_approx(lg - mx);
-                probs[i] = e;
-                sm += e;
-            }
-            m_item = mx;
-            l_item = warp_sum(sm);
-        }
-        __syncwarp();
-
-        // ================= phase 2: P.V ======================================
-        // VQ lanes: (jj, h) = token offset jj in 0..15, channel half h
-        // (channels 64h .. 64h+63 = value groups 2h, 2h+1).
-        const int h = lane & 1, jj = lane >> 1;
+        const float2 ml = softmax_item(
+            probs, p.t1 - p.t0, a.wlog ? a.wlog + (int64_t)p.u * a.l + p.t0 : nullptr, lane);
         float2 vacc[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) vacc[i] = make_float2(0.f, 0.f);
@@ -454,118 +698,16 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_fast_kernel(FastArgs a) 
             uint8_t* slot = wait_slot();
             const JobDesc jd = job_of<B>(a, p, j);
             const float* pr_tok = probs + (jd.ts - p.t0);
-            if (jd.kind == VQ) {
-                const uint8_t* pairs = slot + PB::VQ_TOK * PB::TOK_CODE;
-                if constexpr (B == 2) {
-                    int t = jj;
-                    uint4 cw = make_uint4(0, 0, 0, 0);
-                    float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
-                    float pt = 0.f;
-                    if (t < jd.n) {
-                        cw = *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 16);
-                        pr = *reinterpret_cast<const float4*>(pairs + t * 32 + h * 16);
-                        pt = pr_tok[t];
-                    }
-                    for (; t < jd.n; t += 16) {
-                        // prefetch the next token of this lane
-                        const int tn = t + 16;
-                        uint4 cw_n = cw;
-                        float4 pr_n = pr;
-                        float pt_n = pt;
-                        if (tn < jd.n) {
-                            cw_n = *reinterpret_cast<const uint4*>(slot + tn * PB::TOK_CODE + h * 16);
-                            pr_n = *reinterpret_cast<const float4*>(pairs + tn * 32 + h * 16);
-                            pt_n = pr_tok[tn];
-                        }
-                        const float pk = pt * ksc;
-                        const float ws0 = pk * (pr.y - pr.x);
-                        const float ws1 = pk * (pr.w - pr.z);
-                        zacc0 = fmaf(pt, pr.x, zacc0);
-                        zacc1 = fmaf(pt, pr.z, zacc1);
-                        PB::fma_word(vacc, cw.x, ws0);
-                        PB::fma_word(vacc + 8, cw.y, ws0);
-                        PB::fma_word(vacc + 16, cw.z, ws1);
-                        PB::fma_word(vacc + 24, cw.w, ws1);
-                        cw = cw_n;
-                        pr = pr_n;
-                        pt = pt_n;
-                    }
-                } else {
-                    for (int t = jj; t < jd.n; t += 16) {
-                        const float pt = pr_tok[t];
-                        const float4 pr = *reinterpret_cast<const float4*>(pairs + t * 32 + h * 16);
-                        const float pk = pt * ksc;
-                        const float ws0 = pk * (pr.y - pr.x);
-                        const float ws1 = pk * (pr.w - pr.z);
-                        zacc0 = fmaf(pt, pr.x, zacc0);
-                        zacc1 = fmaf(pt, pr.z, zacc1);
-                        const uint4 c0 =
-                            *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 32);
-                        const uint4 c1 =
-                            *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 32 + 16);
-                        PB::fma_word(vacc, c0.x, ws0);
-                        PB::fma_word(vacc + 4, c0.y, ws0);
-                        PB::fma_word(vacc + 8, c0.z, ws0);
-                        PB::fma_word(vacc + 12, c0.w, ws0);
-                        PB::fma_word(vacc + 16, c1.x, ws1);
-                        PB::fma_word(vacc + 20, c1.y, ws1);
-                        PB::fma_word(vacc + 24, c1.z, ws1);
-                        PB::fma_word(vacc + 28, c1.w, ws1);
-                    }
-                }
-            } else {
-                // ---- fp32 value residual rows -> P.V ------------------------
-                for (int r = 0; r < jd.n; ++r) {
-                    const float4 vv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
-                    const float pt = pr_tok[r];
-                    facc.x = fmaf(pt, vv.x, facc.x);
-                    facc.y = fmaf(pt, vv.y, facc.y);
-                    facc.z = fmaf(pt, vv.z, facc.z);
-                    facc.w = fmaf(pt, vv.w, facc.w);
-                }
-            }
-
+            if (jd.kind == VQ)
+                vq_tokens_accumulate<B>(slot, pr_tok, jd.n, ksc, vacc, zacc0, zacc1, lane);
+            else
+                vf_rows_accumulate(slot, pr_tok, jd.n, facc, lane);
             if (j == p.njobs - 1) {
-                // ---- finalize: reduce value accumulators, write the partial -
-                // 32 rows (one per lane) x 64 channels, 16-byte chunks XOR-
-                // swizzled by row so both the writes and the reads are
-                // bank-conflict free.
-                __syncwarp();
-                float4* red = reinterpret_cast<float4*>(slot);
-#pragma unroll
-                for (int qc = 0; qc < 16; ++qc)
-                    red[lane * 16 + (qc ^ (lane & 7))] =
-                        make_float4(vacc[2 * qc].x, vacc[2 * qc].y, vacc[2 * qc + 1].x,
-                                    vacc[2 * qc + 1].y);
-                float z0 = zacc0, z1 = zacc1;
-#pragma unroll
-                for (int o = 2; o < 32; o <<= 1) {
-                    z0 += __shfl_xor_sync(0xffffffffu, z0, o);
-                    z1 += __shfl_xor_sync(0xffffffffu, z1, o);
-                }
-                __syncwarp();
-                const int ho = lane >> 4;      // output channel half of this lane
-                const int qc = lane & 15;      // 16-byte chunk within the half
-                const float zh0 = __shfl_sync(0xffffffffu, z0, ho);
-                const float zh1 = __shfl_sync(0xffffffffu, z1, ho);
-                const float z = ((lane >> 3) & 1) ? zh1 : zh0;
-                float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int r2 = 0; r2 < 16; ++r2) {
-                    const int row = r2 * 2 + ho;
-                    const float4 v = red[row * 16 + (qc ^ (row & 7))];
-                    s4.x += v.x; s4.y += v.y; s4.z += v.z; s4.w += v.w;
-                }
-                const int m0 = (4 * qc) & 31;  // channel within its 32-channel group
-                float4 o;
-                o.x = fmaf(s4.x, unscale_pos(PB::epos((m0 + 0) % PB::TPW)), z) + facc.x;
-                o.y = fmaf(s4.y, unscale_pos(PB::epos((m0 + 1) % PB::TPW)), z) + facc.y;
-                o.z = fmaf(s4.z, unscale_pos(PB::epos((m0 + 2) % PB::TPW)), z) + facc.z;
-                o.w = fmaf(s4.w, unscale_pos(PB::epos((m0 + 3) % PB::TPW)), z) + facc.w;
-                reinterpret_cast<float4*>(a.part_o + (int64_t)item * D)[lane] = o;
-                if (lane == 0) a.part_ml[item] = make_float2(m_item, l_item);
+                const int64_t pi = (int64_t)p.u * a.n_sub + p.k;
+                v_finalize<B>(slot, vacc, zacc0, zacc1, facc, ml, a.part_o + pi * D,
+                              a.part_ml + pi, lane);
             }
-            release_slot(j == p.njobs - 1);
+            release_slot();
         }
     }
 }

@@ -100,6 +100,18 @@ struct kivi_cache {
     int64_t main_launches = 0;
     int64_t total_launches = 0;
 
+    std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t take_event() {
+        if (event_pool.empty()) {
+            cudaEvent_t e = nullptr;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+
     int64_t kg() const { return l - l % cfg.residual_length; }
     int64_t vg() const { return l - std::min<int64_t>(l, cfg.residual_length); }
 };
@@ -245,14 +257,15 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int B, int NSLOT>
+template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st) {
-    using WS = fast::WarpSmem<NSLOT>;
     const int64_t U = h->n_units;
     if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
+    // body = whole 256-token sub-chunks below floor32(vg) (all quantized)
+    const int64_t nfull = ((h->vg() / 32) * 32) / fast::SUB;
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub);
@@ -266,41 +279,57 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     a.kg = (int)h->kg();
     a.vg = (int)h->vg();
     a.n_sub = (int)n_sub;
-    a.n_items = (int)(U * n_sub);
     a.q = q;
     a.qscale = qscale;
     a.part_o = h->part_o;
     a.part_ml = h->part_ml;
     a.wlog = weights;
 
-    const int smem = WS::STRIDE * fast::WARPS;
-    if (h->fast_per_sm[B][NSLOT] == 0) {
-        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_fast_kernel<B, NSLOT>,
+    const int smem = fast::WS2::STRIDE * fast::WARPS;
+    if (h->fast_per_sm[B][0] == 0) {
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<B>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, fast::attend_fast_kernel<B, NSLOT>, fast::WARPS * 32, smem));
-        h->fast_per_sm[B][NSLOT] = per_sm < 1 ? 1 : per_sm;
+            &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32, smem));
+        h->fast_per_sm[B][0] = per_sm < 1 ? 1 : per_sm;
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
+        h->fast_per_sm[B][1] = per_sm < 1 ? 1 : per_sm;
     }
-    const int per_sm = h->fast_per_sm[B][NSLOT];
-    const int64_t items = U * n_sub;
-    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
-                                           ceil_div(items, fast::WARPS));
-
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->profile) {
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
+        e0 = h->take_event();
+        e1 = h->take_event();
         cudaEventRecord(e0, st);
     }
-    fast::attend_fast_kernel<B, NSLOT><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
-    KIVI_LAUNCHED();
+    if (n_sub > nfull) {
+        a.k_first = (int)nfull;
+        a.n_per_unit = (int)(n_sub - nfull);
+        a.n_items = (int)(U * a.n_per_unit);
+        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][1],
+                                               ceil_div(a.n_items, fast::WARPS));
+        fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    if (nfull > 0) {
+        a.k_first = 0;
+        a.n_per_unit = (int)nfull;
+        a.n_items = (int)(U * nfull);
+        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
+                                               ceil_div(a.n_items, fast::WARPS));
+        fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
     if (h->profile) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
     }
     h->main_launches++;
-    h->total_launches++;
     fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
                                                           weights ? h->stats : nullptr);
     KIVI_LAUNCHED();
@@ -334,8 +363,8 @@ kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, f
     const size_t smem = sizeof(float) * (size_t)(h->cfg.head_dim + 32);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->profile) {
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
+        e0 = h->take_event();
+        e1 = h->take_event();
         cudaEventRecord(e0, st);
     }
     attend_generic_kernel<<<(unsigned)rows, 256, smem, st>>>(a);
@@ -405,6 +434,7 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
     }
+    for (auto e : h->event_pool) cudaEventDestroy(e);
     delete h;
     return KIVI_OK;
 }
@@ -586,8 +616,8 @@ kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float
     if (fast_ok && h->attend_path != 1) {
         const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
         const float qscale = scale * fast::LOG2E;
-        if (h->cfg.bits == 2) return launch_fast<2, 2>(h, t_q, out, weights, qscale, st);
-        return launch_fast<4, 2>(h, t_q, out, weights, qscale, st);
+        if (h->cfg.bits == 2) return launch_fast<2>(h, t_q, out, weights, qscale, st);
+        return launch_fast<4>(h, t_q, out, weights, qscale, st);
     }
     return launch_generic(h, t_q, q_per_kv, out, weights, scale_logits, st);
 }
@@ -957,8 +987,8 @@ kivi_status kivi_profile_read(kivi_cache* h, double* main_kernel_ms, int64_t* ma
         float t = 0.f;
         KIVI_CUDA(cudaEventElapsedTime(&t, ev.first, ev.second));
         ms += t;
-        cudaEventDestroy(ev.first);
-        cudaEventDestroy(ev.second);
+        h->event_pool.push_back(ev.first);
+        h->event_pool.push_back(ev.second);
     }
     h->events.clear();
     if (main_kernel_ms) *main_kernel_ms = ms;
