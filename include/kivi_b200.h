@@ -14,9 +14,11 @@
  *     (cudaMalloc'd, or any memory the GPU can dereference); work is enqueued
  *     on `stream` (a cudaStream_t passed as void*; NULL = legacy default
  *     stream) and the call returns without synchronising.
- *   - `_host` entry points take HOST pointers, stage them through the cache's
- *     pinned/device buffers inside the call, and synchronise `stream` before
- *     returning (the results are in the host buffers on return).
+ *   - `_host` entry points take HOST pointers and enqueue the host<->device
+ *     copies on `stream` together with the kernels (cudaMemcpyAsync
+ *     semantics: use pinned buffers for asynchrony and synchronise `stream`
+ *     before reading outputs or reusing inputs).  kivi_prefill_host
+ *     synchronises before returning.
  *   - Errors mirror the reference's exception types (reference
  *     proj/include/kivi/errors.hpp:10-22): a failing call returns a status
  *     and leaves the cache unchanged; kivi_last_error() returns a
@@ -147,7 +149,7 @@ kivi_status kivi_decode(kivi_cache* cache, const float* t_q, const float* t_k, c
                         int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
                         void* stream);
 
-/* Host-buffer variants: copies in and out happen inside the call. */
+/* Host-buffer variants: the copies in and out are enqueued with the work. */
 kivi_status kivi_prefill_host(kivi_cache* cache, const float* keys, const float* values,
                               int64_t l, void* stream);
 kivi_status kivi_append_host(kivi_cache* cache, const float* t_k, const float* t_v,
@@ -185,6 +187,16 @@ kivi_status kivi_dequantize_matrix(const uint8_t* packed, const double* zero_poi
                                    const double* scales, int64_t rows, int64_t cols,
                                    int32_t bits, int64_t group_size, kivi_axis axis, float* out,
                                    void* stream);
+/* Unpacked-code variants for ANY B in [1, 8] (reference quantize_grouped /
+ * dequantize_grouped, quantize.cpp:105-167, used by quantize_group and
+ * fake_quantize which accept non-packable B): one uint8 code per element, in
+ * group order.  Device pointers. */
+kivi_status kivi_quantize_codes(const float* m, int64_t rows, int64_t cols, int32_t bits,
+                                int64_t group_size, kivi_axis axis, uint8_t* codes,
+                                double* zero_points, double* scales, void* stream);
+kivi_status kivi_dequantize_codes(const uint8_t* codes, const double* zero_points,
+                                  const double* scales, int64_t rows, int64_t cols,
+                                  int64_t group_size, kivi_axis axis, float* out, void* stream);
 /* pack_codes / unpack_codes (quantize.cpp:59-93).  pack returns
  * KIVI_ERR_USAGE for bits not in {1,2,4,8} or a code > 2^B-1 (after
  * synchronising `stream` to inspect the device-side range check). */

@@ -278,6 +278,55 @@ __global__ void quantize_matrix_kernel(const float* __restrict__ m, int64_t rows
     }
 }
 
+// Unpacked variant for any B in [1, 8]: codes[g*G + i] = code of element i
+// of group g (reference quantize_grouped, quantize.cpp:105-140).
+__global__ void quantize_codes_kernel(const float* __restrict__ m, int64_t rows, int64_t cols,
+                                      int bits, int G, int per_channel, uint8_t* __restrict__ codes,
+                                      double* __restrict__ zp, double* __restrict__ sc) {
+    const int maxc = (1 << bits) - 1;
+    const int64_t ngroups = rows * cols / G;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const float* src;
+        int64_t stride;
+        if (per_channel) {
+            const int64_t tg = g / cols, ch = g % cols;
+            src = m + tg * G * cols + ch;
+            stride = cols;
+        } else {
+            const int64_t gpr = cols / G;
+            src = m + (g / gpr) * cols + (g % gpr) * G;
+            stride = 1;
+        }
+        float lo = src[0], hi = src[0];
+        for (int i = 1; i < G; ++i) minmax_step(src[(int64_t)i * stride], lo, hi);
+        const CodeCtx cc = make_code_ctx(lo, hi, maxc);
+        for (int i = 0; i < G; ++i) codes[g * G + i] = (uint8_t)quant_code(cc, src[(int64_t)i * stride]);
+        zp[g] = (double)lo;
+        sc[g] = cc.s;
+    }
+}
+
+__global__ void dequantize_codes_kernel(const uint8_t* __restrict__ codes,
+                                        const double* __restrict__ zp,
+                                        const double* __restrict__ sc, int64_t rows, int64_t cols,
+                                        int G, int per_channel, float* __restrict__ out) {
+    const int64_t n = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / cols, ch = e % cols;
+        int64_t g, pos;
+        if (per_channel) {
+            g = (r / G) * cols + ch;
+            pos = g * G + r % G;
+        } else {
+            g = r * (cols / G) + ch / G;
+            pos = e;
+        }
+        out[e] = dequant_exact(codes[pos], sc[g], zp[g]);
+    }
+}
+
 // QuantizedTensor::dequantize: one thread per element.
 __global__ void dequantize_matrix_kernel(const uint8_t* __restrict__ packed,
                                          const double* __restrict__ zp,

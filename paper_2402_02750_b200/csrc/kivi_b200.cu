@@ -64,6 +64,31 @@ cudaError_t dalloc(T** p, size_t count) {
     return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 
+// Grow-only per-thread device scratch (standalone entry points): avoids
+// cudaMalloc/cudaFree (which synchronises the device) on every call.
+struct Scratch {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = 256;
+        while (want < bytes) want <<= 1;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+};
+Scratch& scratch(int slot) {
+    thread_local Scratch s[4];
+    return s[slot];
+}
+
 }  // namespace
 
 struct kivi_cache {
@@ -93,6 +118,8 @@ struct kivi_cache {
     float* st_out = nullptr;
     float* st_w = nullptr;
     int64_t st_cap_q = 0, st_cap_out = 0, st_cap_k = 0, st_cap_v = 0, st_cap_w = 0;
+    double* xfer = nullptr;  // export/import staging
+    int64_t xfer_cap = 0;
 
     // profiling
     bool profile = false;
@@ -430,6 +457,7 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     cudaFree(h->st_v);
     cudaFree(h->st_out);
     cudaFree(h->st_w);
+    cudaFree(h->xfer);
     for (auto& ev : h->events) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
@@ -715,9 +743,11 @@ kivi_status kivi_export_unit(const kivi_cache* h, int64_t unit, kivi_unit_state*
     const int64_t d = h->cfg.head_dim, G = h->cfg.group_size, B = h->cfg.bits;
     const int64_t kgroups = kg * d / G, vgroups = vg * d / G;
     const int64_t kr = l - kg, vr = l - vg;
-    double* tmp = nullptr;
     const int64_t ntmp = 2 * (kgroups + vgroups) + (kr + vr) * d / 2 + 8;
-    KIVI_CUDA(dalloc(&tmp, (size_t)ntmp));
+    kivi_cache* hm = const_cast<kivi_cache*>(h);
+    kivi_status rc = ensure(&hm->xfer, &hm->xfer_cap, ntmp);
+    if (rc) return rc;
+    double* tmp = hm->xfer;
     double *kz = tmp, *ks = kz + kgroups, *vz = ks + kgroups, *vs = vz + vgroups;
     float* kres = reinterpret_cast<float*>(vs + vgroups);
     float* vres = kres + kr * d;
@@ -756,7 +786,6 @@ kivi_status kivi_export_unit(const kivi_cache* h, int64_t unit, kivi_unit_state*
         KIVI_CUDA(cudaMemcpyAsync(dst->value_residual, vres, sizeof(float) * vr * d,
                                   cudaMemcpyDeviceToHost, st));
     cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(tmp);
     if (e != cudaSuccess) return fail(KIVI_ERR_CUDA, "export: %s", cudaGetErrorString(e));
     return KIVI_OK;
 }
@@ -792,9 +821,10 @@ kivi_status kivi_import_unit(kivi_cache* h, int64_t unit, int64_t total_tokens,
     if (vbytes)
         KIVI_CUDA(cudaMemcpyAsync(c.vcodes + unit * c.v_ustride, src->value_packed, vbytes,
                                   cudaMemcpyHostToDevice, st));
-    double* tmp = nullptr;
     const int64_t ntmp = 2 * (kgroups + vgroups) + (kr + vr) * d / 2 + 8;
-    KIVI_CUDA(dalloc(&tmp, (size_t)ntmp));
+    rc = ensure(&h->xfer, &h->xfer_cap, ntmp);
+    if (rc) return rc;
+    double* tmp = h->xfer;
     double *kz = tmp, *ks = kz + kgroups, *vz = ks + kgroups, *vs = vz + vgroups;
     float* kres = reinterpret_cast<float*>(vs + vgroups);
     float* vres = kres + kr * d;
@@ -821,7 +851,6 @@ kivi_status kivi_import_unit(kivi_cache* h, int64_t unit, int64_t total_tokens,
     }
     KIVI_LAUNCHED();
     cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(tmp);
     if (e != cudaSuccess) return fail(KIVI_ERR_CUDA, "import: %s", cudaGetErrorString(e));
     return KIVI_OK;
 }
@@ -856,15 +885,14 @@ kivi_status kivi_quantize_matrix(const float* m, int64_t rows, int64_t cols, int
     if (rows * cols == 0) return KIVI_OK;
     cudaStream_t st = S(stream);
     const int64_t nbytes = ceil_div(rows * cols * bits, 8);
-    uint8_t* tmp = nullptr;
-    KIVI_CUDA(dalloc(&tmp, (size_t)round_up(nbytes, 4)));
+    KIVI_CUDA(scratch(0).ensure((size_t)round_up(nbytes, 4)));
+    uint8_t* tmp = static_cast<uint8_t*>(scratch(0).p);
     KIVI_CUDA(cudaMemsetAsync(tmp, 0, (size_t)round_up(nbytes, 4), st));
     quantize_matrix_kernel<<<grid_for(rows * cols / group_size), 256, 0, st>>>(
         m, rows, cols, bits, (int)group_size, axis == KIVI_PER_CHANNEL, tmp, zero_points, scales);
     cudaError_t le = cudaGetLastError();
     cudaError_t ce = cudaMemcpyAsync(packed, tmp, (size_t)nbytes, cudaMemcpyDefault, st);
     cudaError_t se = cudaStreamSynchronize(st);
-    cudaFree(tmp);
     if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(le));
     if (ce != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(ce));
     if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "quantize: %s", cudaGetErrorString(se));
@@ -881,17 +909,46 @@ kivi_status kivi_dequantize_matrix(const uint8_t* packed, const double* zero_poi
     // read_code views the stream as 32-bit words: stage into a padded buffer.
     cudaStream_t st = S(stream);
     const int64_t nbytes = ceil_div(rows * cols * bits, 8);
-    uint8_t* tmp = nullptr;
-    KIVI_CUDA(dalloc(&tmp, (size_t)round_up(nbytes, 4)));
+    KIVI_CUDA(scratch(1).ensure((size_t)round_up(nbytes, 4)));
+    uint8_t* tmp = static_cast<uint8_t*>(scratch(1).p);
     KIVI_CUDA(cudaMemsetAsync(tmp, 0, (size_t)round_up(nbytes, 4), st));
     KIVI_CUDA(cudaMemcpyAsync(tmp, packed, (size_t)nbytes, cudaMemcpyDefault, st));
     dequantize_matrix_kernel<<<grid_for(rows * cols), 256, 0, st>>>(
         tmp, zero_points, scales, rows, cols, bits, (int)group_size, axis == KIVI_PER_CHANNEL, out);
     cudaError_t le = cudaGetLastError();
     cudaError_t se = cudaStreamSynchronize(st);
-    cudaFree(tmp);
     if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "dequantize: %s", cudaGetErrorString(le));
     if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "dequantize: %s", cudaGetErrorString(se));
+    return KIVI_OK;
+}
+
+kivi_status kivi_quantize_codes(const float* m, int64_t rows, int64_t cols, int32_t bits,
+                                int64_t group_size, kivi_axis axis, uint8_t* codes,
+                                double* zero_points, double* scales, void* stream) {
+    if (bits < 1 || bits > 8) return fail(KIVI_ERR_CONFIG, "bits must be in [1, 8], got %d", bits);
+    if (group_size < 1) return fail(KIVI_ERR_CONFIG, "group_size must be >= 1");
+    const int64_t extent = axis == KIVI_PER_CHANNEL ? rows : cols;
+    if (extent % group_size != 0)
+        return fail(KIVI_ERR_SHAPE,
+                    "quantize: %s grouped axis extent %lld not divisible by group size %lld "
+                    "(matrix %lldx%lld)",
+                    axis == KIVI_PER_CHANNEL ? "per_channel" : "per_token", (long long)extent,
+                    (long long)group_size, (long long)rows, (long long)cols);
+    if (rows * cols == 0) return KIVI_OK;
+    quantize_codes_kernel<<<grid_for(rows * cols / group_size), 256, 0, S(stream)>>>(
+        m, rows, cols, bits, (int)group_size, axis == KIVI_PER_CHANNEL, codes, zero_points, scales);
+    KIVI_LAUNCHED();
+    return KIVI_OK;
+}
+
+kivi_status kivi_dequantize_codes(const uint8_t* codes, const double* zero_points,
+                                  const double* scales, int64_t rows, int64_t cols,
+                                  int64_t group_size, kivi_axis axis, float* out, void* stream) {
+    if (group_size < 1) return fail(KIVI_ERR_CONFIG, "group_size must be >= 1");
+    if (rows * cols == 0) return KIVI_OK;
+    dequantize_codes_kernel<<<grid_for(rows * cols), 256, 0, S(stream)>>>(
+        codes, zero_points, scales, rows, cols, (int)group_size, axis == KIVI_PER_CHANNEL, out);
+    KIVI_LAUNCHED();
     return KIVI_OK;
 }
 
@@ -901,15 +958,14 @@ kivi_status kivi_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8
         return fail(KIVI_ERR_USAGE, "pack_codes: bits must be one of {1,2,4,8}, got %d", bits);
     if (n == 0) return KIVI_OK;
     cudaStream_t st = S(stream);
-    int* bad = nullptr;
-    KIVI_CUDA(dalloc(&bad, 1));
+    KIVI_CUDA(scratch(2).ensure(sizeof(int)));
+    int* bad = static_cast<int*>(scratch(2).p);
     KIVI_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
     pack_codes_kernel<<<grid_for(ceil_div(n * bits, 8)), 256, 0, st>>>(codes, n, bits, bytes, bad);
     int hbad = 0;
     cudaError_t le = cudaGetLastError();
     cudaError_t ce = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaError_t se = cudaStreamSynchronize(st);
-    cudaFree(bad);
     if (le != cudaSuccess || ce != cudaSuccess || se != cudaSuccess)
         return fail(KIVI_ERR_CUDA, "pack_codes: %s",
                     cudaGetErrorString(le != cudaSuccess ? le : (ce != cudaSuccess ? ce : se)));
@@ -933,8 +989,8 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
     if (n_q < 1 || d < 1) return fail(KIVI_ERR_SHAPE, "reference_attention: empty query");
     if (l < 1) return fail(KIVI_ERR_SHAPE, "reference_attention: empty keys");
     cudaStream_t st = S(stream);
-    float* scratch = nullptr;
-    KIVI_CUDA(dalloc(&scratch, (size_t)(n_q * l)));
+    KIVI_CUDA(scratch(3).ensure(sizeof(float) * (size_t)(n_q * l)));
+    float* lg_scratch = static_cast<float*>(scratch(3).p);
     AttendGenericArgs a{};
     a.c.bits = 2;
     a.c.G = 1;
@@ -953,12 +1009,11 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
     a.qpk = (int)n_q;
     a.out = out;
     a.weights = nullptr;
-    a.scratch = scratch;
+    a.scratch = lg_scratch;
     a.scale_logits = scale_logits;
     attend_generic_kernel<<<(unsigned)n_q, 256, sizeof(float) * (size_t)(d + 32), st>>>(a);
     cudaError_t le = cudaGetLastError();
     cudaError_t se = cudaStreamSynchronize(st);
-    cudaFree(scratch);
     if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(le));
     if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(se));
     return KIVI_OK;
