@@ -240,18 +240,34 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
     }
 }
 
-// fp32 key residual rows -> logits.
+// fp32 key residual rows -> logits.  16 independent partial dot products
+// (lane owns channels 4*lane..4*lane+3), then one xor-16 step and a
+// reduce-scatter over 16 lanes, after which lane r (< 16) holds row r.
 __device__ __forceinline__ void kf_rows_to_logits(const uint8_t* slot, const float* qq,
                                                   float* probs_dst, int n, int lane) {
     const float4 qa = reinterpret_cast<const float4*>(qq)[lane];
-    float mine = 0.f;
-    for (int r = 0; r < n; ++r) {
-        const float4 kv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
-        float v = qa.x * kv.x + qa.y * kv.y + qa.z * kv.z + qa.w * kv.w;
-        v = warp_sum(v);
-        if (lane == r) mine = v;
+    float part[F_ROWS];
+#pragma unroll
+    for (int r = 0; r < F_ROWS; ++r) {
+        part[r] = 0.f;
+        if (r < n) {
+            const float4 kv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
+            part[r] = qa.x * kv.x + qa.y * kv.y + qa.z * kv.z + qa.w * kv.w;
+        }
     }
-    if (lane < n) probs_dst[lane] = mine;
+#pragma unroll
+    for (int r = 0; r < F_ROWS; ++r) part[r] += __shfl_xor_sync(0xffffffffu, part[r], 16);
+#pragma unroll
+    for (int half = F_ROWS / 2; half >= 1; half >>= 1) {
+        const bool upper = (lane & half) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = upper ? part[i] : part[i + half];
+            const float keep = upper ? part[i + half] : part[i];
+            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+        }
+    }
+    if (lane < n) probs_dst[lane] = part[0];
 }
 
 // Softmax over the item's logits (in place, log2 domain); returns (max, sum).
@@ -341,14 +357,30 @@ __device__ __forceinline__ void vq_tokens_accumulate(const uint8_t* slot, const 
 // fp32 value residual rows -> P.V (lane owns channels 4*lane .. 4*lane+3).
 __device__ __forceinline__ void vf_rows_accumulate(const uint8_t* slot, const float* pr_tok, int n,
                                                    float4& facc, int lane) {
-    for (int r = 0; r < n; ++r) {
-        const float4 vv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
-        const float pt = pr_tok[r];
-        facc.x = fmaf(pt, vv.x, facc.x);
-        facc.y = fmaf(pt, vv.y, facc.y);
-        facc.z = fmaf(pt, vv.z, facc.z);
-        facc.w = fmaf(pt, vv.w, facc.w);
+    float4 a2 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < F_ROWS; r += 2) {
+        if (r < n) {
+            const float4 vv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
+            const float pt = pr_tok[r];
+            facc.x = fmaf(pt, vv.x, facc.x);
+            facc.y = fmaf(pt, vv.y, facc.y);
+            facc.z = fmaf(pt, vv.z, facc.z);
+            facc.w = fmaf(pt, vv.w, facc.w);
+        }
+        if (r + 1 < n) {
+            const float4 vv = reinterpret_cast<const float4*>(slot + (r + 1) * D * 4)[lane];
+            const float pt = pr_tok[r + 1];
+            a2.x = fmaf(pt, vv.x, a2.x);
+            a2.y = fmaf(pt, vv.y, a2.y);
+            a2.z = fmaf(pt, vv.z, a2.z);
+            a2.w = fmaf(pt, vv.w, a2.w);
+        }
     }
+    facc.x += a2.x;
+    facc.y += a2.y;
+    facc.z += a2.z;
+    facc.w += a2.w;
 }
 
 // Reduce the value accumulators across the 16 lanes sharing a channel half

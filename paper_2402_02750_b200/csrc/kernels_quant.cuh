@@ -164,6 +164,95 @@ __global__ void append_kernel(CacheDev c, const float* __restrict__ tk,
     }
 }
 
+// ---- fast append for d = 128, G = 32, B in {2, 4} (one warp per unit) -----
+// Same semantics as append_kernel.  Lane j owns channels 4j..4j+3 of a row;
+// a 32-channel value group is 8 lanes.  Ties in the group min / max follow
+// std::minmax_element (first smallest, last largest) via the channel index.
+__device__ __forceinline__ void minmax_pair_reduce8(float& lo, int& ilo, float& hi, int& ihi) {
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const float olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const int oilo = __shfl_xor_sync(0xffffffffu, ilo, o);
+        const float ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const int oihi = __shfl_xor_sync(0xffffffffu, ihi, o);
+        if (olo < lo || (!(lo < olo) && oilo < ilo)) { lo = olo; ilo = oilo; }
+        if (ohi > hi || (!(hi > ohi) && oihi > ihi)) { hi = ohi; ihi = oihi; }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const float* __restrict__ tk,
+                                                          const float* __restrict__ tv, int64_t l) {
+    constexpr int D = 128, G = 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (u >= c.n_units) return;
+    const int R = c.R;
+    const int slot = (int)(l % R);
+    float* kring = c.kring + u * c.ring_ustride;
+    float* vring = c.vring + u * c.ring_ustride;
+    const float4 kv = reinterpret_cast<const float4*>(tk + u * D)[lane];
+    const float4 vv = reinterpret_cast<const float4*>(tv + u * D)[lane];
+    reinterpret_cast<float4*>(kring + (int64_t)slot * D)[lane] = kv;
+
+    if (l >= R) {
+        // value FIFO pop: quantize the oldest row (token l - R) per-token
+        const int64_t e = l - R;
+        const float4 old = reinterpret_cast<const float4*>(vring + (int64_t)slot * D)[lane];
+        const float x[4] = {old.x, old.y, old.z, old.w};
+        float lo = x[0], hi = x[0];
+        int ilo = 4 * lane, ihi = 4 * lane;
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+            if (x[i] < lo) { lo = x[i]; ilo = 4 * lane + i; }
+            if (!(x[i] < hi)) { hi = x[i]; ihi = 4 * lane + i; }
+        }
+        minmax_pair_reduce8(lo, ilo, hi, ihi);
+        const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+        uint32_t bits = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bits |= quant_code(cc, x[i]) << (B * i);
+        // lane's 4 codes -> position (4*lane*B) of the token's 128*B-bit row
+        uint32_t word = bits << ((4 * lane * B) & 31);
+        constexpr int LPW = 32 / (4 * B);  // lanes sharing one 32-bit word
+#pragma unroll
+        for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+        uint32_t* vw = reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + e * (D * B / 32);
+        if ((lane % LPW) == 0) vw[(4 * lane * B) >> 5] = word;
+        if ((lane & 7) == 0) c.vpairs[u * c.vp_ustride + e * (D / G) + (lane >> 3)] = make_float2(lo, hi);
+    }
+    reinterpret_cast<float4*>(vring + (int64_t)slot * D)[lane] = vv;
+
+    if ((l + 1) % R == 0) {
+        // key flush: quantize the R x 128 ring per-channel into R/32 tiles;
+        // lane owns channels lane, lane+32, lane+64, lane+96 (sequential over
+        // the 32 tokens of a group: exact first-min / last-max order).
+        __syncwarp();
+        const int64_t tile0 = (l + 1 - R) / G;
+        uint32_t* kw = reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride);
+        for (int tl = 0; tl < R / G; ++tl) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ch = lane + 32 * q;
+                const float* col = kring + (int64_t)tl * G * D + ch;
+                float lo = col[0], hi = col[0];
+                for (int i = 1; i < G; ++i) minmax_step(col[(int64_t)i * D], lo, hi);
+                const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+                const int64_t g = (tile0 + tl) * D + ch;
+                constexpr int CPW = 32 / B;  // codes per word
+#pragma unroll
+                for (int w = 0; w < G / CPW; ++w) {
+                    uint32_t word = 0;
+                    for (int i = 0; i < CPW; ++i)
+                        word |= quant_code(cc, col[(int64_t)(w * CPW + i) * D]) << (B * i);
+                    kw[g * (G / CPW) + w] = word;
+                }
+                c.kpairs[u * c.kp_ustride + g] = make_float2(lo, hi);
+            }
+        }
+    }
+}
+
 // ---- materialize (reference materialize_*, kv_cache.cpp:100-106) ---------
 __global__ void materialize_kernel(CacheDev c, int64_t l, int64_t kg, int64_t vg,
                                    float* __restrict__ kout, float* __restrict__ vout) {

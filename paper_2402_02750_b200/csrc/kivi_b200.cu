@@ -120,6 +120,11 @@ struct kivi_cache {
     int64_t st_cap_q = 0, st_cap_out = 0, st_cap_k = 0, st_cap_v = 0, st_cap_w = 0;
     double* xfer = nullptr;  // export/import staging
     int64_t xfer_cap = 0;
+    // host-buffer path: inputs are uploaded on a private copy stream so the
+    // next call's upload overlaps this call's kernels
+    cudaStream_t h2d = nullptr;
+    cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
+    cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
 
     // profiling
     bool profile = false;
@@ -357,6 +362,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         h->events.emplace_back(e0, e1);
     }
     h->main_launches++;
+    // K5: merge the per-item partials (a separate launch keeps the merge work
+    // balanced; fusing it into the attend tail serialised it on the last warps)
     fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
                                                           weights ? h->stats : nullptr);
     KIVI_LAUNCHED();
@@ -458,6 +465,9 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     cudaFree(h->st_out);
     cudaFree(h->st_w);
     cudaFree(h->xfer);
+    if (h->h2d) cudaStreamDestroy(h->h2d);
+    if (h->ev_in_free) cudaEventDestroy(h->ev_in_free);
+    if (h->ev_h2d_done) cudaEventDestroy(h->ev_h2d_done);
     for (auto& ev : h->events) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
@@ -617,7 +627,16 @@ kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void*
     cudaStream_t st = S(stream);
     kivi_status rc = ensure_capacity(h, h->l + 1, st);
     if (rc) return rc;
-    append_kernel<<<(unsigned)h->n_units, 128, 0, st>>>(h->dev, t_k, t_v, h->l);
+    const kivi_config& cf = h->cfg;
+    if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4)) {
+        const unsigned grid = (unsigned)ceil_div(h->n_units, 8);
+        if (cf.bits == 2)
+            append_fast_kernel<2><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
+        else
+            append_fast_kernel<4><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
+    } else {
+        append_kernel<<<(unsigned)h->n_units, 128, 0, st>>>(h->dev, t_k, t_v, h->l);
+    }
     KIVI_LAUNCHED();
     h->total_launches++;
     const int64_t R = h->cfg.residual_length;
@@ -685,6 +704,12 @@ kivi_status kivi_prefill_host(kivi_cache* h, const float* keys, const float* val
 static kivi_status stage_rows(kivi_cache* h, int64_t qpk, int64_t wlen) {
     const int64_t U = h->n_units, d = h->cfg.head_dim;
     kivi_status rc;
+    if (!h->h2d) {
+        KIVI_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_in_free, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_h2d_done, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventRecord(h->ev_in_free, h->h2d));  // nothing staged yet
+    }
     if ((rc = ensure(&h->st_q, &h->st_cap_q, U * qpk * d))) return rc;
     if ((rc = ensure(&h->st_out, &h->st_cap_out, U * qpk * d))) return rc;
     if ((rc = ensure(&h->st_k, &h->st_cap_k, U * d))) return rc;
@@ -701,9 +726,15 @@ kivi_status kivi_append_host(kivi_cache* h, const float* t_k, const float* t_v, 
     if (rc) return rc;
     cudaStream_t st = S(stream);
     const size_t bytes = sizeof(float) * (size_t)(h->n_units * h->cfg.head_dim);
-    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, bytes, cudaMemcpyHostToDevice, st));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, bytes, cudaMemcpyHostToDevice, st));
-    return kivi_append(h, h->st_k, h->st_v, stream);
+    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_in_free, 0));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, bytes, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, bytes, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaEventRecord(h->ev_h2d_done, h->h2d));
+    KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_h2d_done, 0));
+    rc = kivi_append(h, h->st_k, h->st_v, stream);
+    if (rc) return rc;
+    KIVI_CUDA(cudaEventRecord(h->ev_in_free, st));
+    return KIVI_OK;
 }
 
 kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, const float* t_v,
@@ -718,13 +749,18 @@ kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, 
     kivi_status rc = stage_rows(h, q_per_kv, wlen);
     if (rc) return rc;
     cudaStream_t st = S(stream);
+    // upload on the copy stream once the previous call's kernels consumed the staging
+    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_in_free, 0));
     KIVI_CUDA(cudaMemcpyAsync(h->st_q, t_q, sizeof(float) * U * q_per_kv * d,
-                              cudaMemcpyHostToDevice, st));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, sizeof(float) * U * d, cudaMemcpyHostToDevice, st));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, st));
+                              cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaEventRecord(h->ev_h2d_done, h->h2d));
+    KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_h2d_done, 0));
     rc = kivi_decode(h, h->st_q, h->st_k, h->st_v, q_per_kv, h->st_out, weights ? h->st_w : nullptr,
                      scale_logits, stream);
     if (rc) return rc;
+    KIVI_CUDA(cudaEventRecord(h->ev_in_free, st));
     KIVI_CUDA(cudaMemcpyAsync(out, h->st_out, sizeof(float) * U * q_per_kv * d,
                               cudaMemcpyDeviceToHost, st));
     if (weights)

@@ -1,0 +1,10 @@
+# Full round evidence: tests, smoke, bench (ours + reference arm), ncu launch list + full capture.
+cd "$(dirname "$0")/.." && TAG=${1:-full}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > gpurun_out/gpu_$TAG.txt
+nproc >> gpurun_out/gpu_$TAG.txt; lscpu | grep "Model name" >> gpurun_out/gpu_$TAG.txt
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_$TAG.log 2>&1; echo PYTEST $?; tail -3 gpurun_out/pytest_$TAG.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo SMOKE $?; tail -1 gpurun_out/smoke_$TAG.log
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo BENCH $?; cat gpurun_out/bench_$TAG.json
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2>&1; echo REF $?; cat gpurun_out/bench_ref_$TAG.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1; echo NCU_LAUNCH $?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"attend_(body|tail)" -s 10 -c 2 -o gpurun_out/prof_$TAG python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --layers 6 > gpurun_out/ncu_$TAG.log 2>&1; echo NCU_FULL $?
