@@ -42,6 +42,13 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 #define KIVI_F(x) __uint_as_float(x)
 
+// Unroll factor of the key-tile loop (8 iterations).  Full unrolling costs
+// ~14 KB of SASS; see DESIGN.md for the measured trade-off.
+#ifndef KIVI_KQ_UNROLL
+#define KIVI_KQ_UNROLL 2
+#endif
+constexpr int KQ_UNROLL = KIVI_KQ_UNROLL;
+
 template <int B>
 struct P;
 template <>
@@ -112,6 +119,7 @@ struct FastArgs {
     float* part_o;      // [units][n_sub][128]
     float2* part_ml;    // [units][n_sub]   (max, sum) in log2 domain
     float* wlog;        // [units][l] log2-domain logits, or null
+    int* work;          // body kernel: dynamic item counter (zeroed before launch)
 };
 
 // Per-warp shared memory.  One q staging buffer suffices for NSLOT == 2: the
@@ -162,7 +170,7 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
             uint4 cw = *reinterpret_cast<const uint4*>(codes + b * 16);
             float4 pr = *reinterpret_cast<const float4*>(pairs + b * 16);
             float2 qv = *reinterpret_cast<const float2*>(qq + 2 * b);
-#pragma unroll
+#pragma unroll KQ_UNROLL
             for (int it = 0; it < 8; ++it) {
                 uint4 cw_n = cw;
                 float4 pr_n = pr;
@@ -456,7 +464,17 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     const int nper = a.n_per_unit;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
 
-    int f_item = gw, f_job = 0;
+    // Items are taken dynamically (atomic counter), one item ahead of use, so
+    // CTAs that start late — e.g. after a concurrently running tail kernel
+    // frees their slot — simply take fewer items.
+    auto grab = [&]() -> int {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(a.work, 1);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    int f_item = grab(), f_job = 0;
+    int f_ahead = grab();   // the item after f_item (atomic latency off the critical path)
+    int c_next = f_item;    // next item for the compute loop
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
@@ -487,7 +505,9 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
         }
         if (++f_job == NJ) {
             f_job = 0;
-            f_item += tw;
+            f_item = f_ahead;
+            c_next = f_item;
+            if (f_item < a.n_items) f_ahead = grab();
             f_u = f_item / nper;
             f_k = f_item - f_u * nper;
         }
@@ -508,7 +528,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
         cs ^= 1;
     };
 
-    for (int item = gw; item < a.n_items; item += tw) {
+    for (int item = c_next; item < a.n_items; item = c_next) {
         const int u = item / nper;
         const int k = a.k_first + (item - u * nper);
 #pragma unroll 1

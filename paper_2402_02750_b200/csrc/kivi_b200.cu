@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -123,6 +124,10 @@ struct kivi_cache {
     // host-buffer path: inputs are uploaded on a private copy stream so the
     // next call's upload overlaps this call's kernels
     cudaStream_t h2d = nullptr;
+    // fast attend: the tail kernel runs on a side stream next to the body kernel
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int* work = nullptr;  // body kernel dynamic item counter
     cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
     cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
 
@@ -278,6 +283,13 @@ bool fast_supported(const kivi_cache* h, int qpk) {
     return qpk == 1 && c.head_dim == 128 && c.group_size == 32 && (c.bits == 2 || c.bits == 4);
 }
 
+// Tuning knobs (read once): KIVI_TAIL_SIDE=0 runs the tail kernel on the
+// caller's stream before the body; KIVI_TAIL_CTAS sets its CTAs per SM.
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -337,26 +349,47 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         e1 = h->take_event();
         cudaEventRecord(e0, st);
     }
-    if (n_sub > nfull) {
+    if (!h->side) {
+        KIVI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        KIVI_CUDA(dalloc(&h->work, 1));
+    }
+    const bool has_tail = n_sub > nfull;
+    static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
+    static const int tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
+    cudaStream_t tail_st = (tail_side && nfull > 0) ? h->side : st;
+    if (has_tail) {
+        // Tail items (residual fp32 tokens, latency-bound) on a side stream
+        // with one CTA per SM, concurrently with the ALU-bound body kernel.
+        if (tail_st != st) {
+            KIVI_CUDA(cudaEventRecord(h->ev_fork, st));
+            KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        }
         a.k_first = (int)nfull;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
-        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][1],
+        const int per_sm = (nfull > 0 && tail_st != st) ? tail_ctas : h->fast_per_sm[B][1];
+        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
                                                ceil_div(a.n_items, fast::WARPS));
-        fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
+        fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
         KIVI_LAUNCHED();
+        if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
         h->total_launches++;
     }
     if (nfull > 0) {
         a.k_first = 0;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
+        a.work = h->work;
+        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int), st));
         const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
                                                ceil_div(a.n_items, fast::WARPS));
         fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
+    if (has_tail && tail_st != st) KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
     if (h->profile) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
@@ -466,6 +499,10 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     cudaFree(h->st_w);
     cudaFree(h->xfer);
     if (h->h2d) cudaStreamDestroy(h->h2d);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    cudaFree(h->work);
     if (h->ev_in_free) cudaEventDestroy(h->ev_in_free);
     if (h->ev_h2d_done) cudaEventDestroy(h->ev_h2d_done);
     for (auto& ev : h->events) {
