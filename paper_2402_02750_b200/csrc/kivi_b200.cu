@@ -12,6 +12,7 @@
 #include "../../include/kivi_b200.h"
 #include "common.cuh"
 #include "kernels_attend_fast.cuh"
+#include "kernels_attend_gqa.cuh"
 #include "kernels_attend_generic.cuh"
 #include "kernels_quant.cuh"
 
@@ -280,7 +281,9 @@ kivi_status ensure_capacity(kivi_cache* h, int64_t tokens, cudaStream_t st) {
 
 bool fast_supported(const kivi_cache* h, int qpk) {
     const kivi_config& c = h->cfg;
-    return qpk == 1 && c.head_dim == 128 && c.group_size == 32 && (c.bits == 2 || c.bits == 4);
+    if (c.head_dim != 128 || c.group_size != 32) return false;
+    if (qpk == 1) return c.bits == 2 || c.bits == 4;
+    return c.bits == 2 && (qpk == 2 || qpk == 4);  // GQA kernel
 }
 
 // Tuning knobs (read once): KIVI_TAIL_SIDE=0 runs the tail kernel on the
@@ -404,6 +407,73 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     if (weights) {
         fast::normalize_weights_kernel<<<grid_for(U * h->l), 256, 0, st>>>(weights, h->stats, h->l,
                                                                             U);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    return KIVI_OK;
+}
+
+template <int H>
+kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
+                       cudaStream_t st) {
+    using WS = gqa::GS<H>;
+    const int64_t U = h->n_units;
+    if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
+        return fail(KIVI_ERR_CONFIG, "GQA attend path: cache too large for 32-bit indexing");
+    const int64_t n_sub = ceil_div(h->l, fast::SUB);
+    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * H * fast::D);
+    if (rc) return rc;
+    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub * H);
+    if (rc) return rc;
+    rc = ensure(&h->stats, &h->stats_cap, U * H);
+    if (rc) return rc;
+    fast::FastArgs a{};
+    a.c = h->dev;
+    a.l = (int)h->l;
+    a.kg = (int)h->kg();
+    a.vg = (int)h->vg();
+    a.n_sub = (int)n_sub;
+    a.k_first = 0;
+    a.n_per_unit = (int)n_sub;
+    a.n_items = (int)(U * n_sub);
+    a.q = q;
+    a.qscale = qscale;
+    a.part_o = h->part_o;
+    a.part_ml = h->part_ml;
+    a.wlog = weights;
+    const int smem = WS::STRIDE * gqa::WARPS;
+    const int key = 4 + H;
+    if (h->fast_per_sm[key][2] == 0) {
+        KIVI_CUDA(cudaFuncSetAttribute(gqa::attend_gqa_kernel<H>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, gqa::attend_gqa_kernel<H>, gqa::WARPS * 32, smem));
+        h->fast_per_sm[key][2] = per_sm < 1 ? 1 : per_sm;
+    }
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][2],
+                                           ceil_div(a.n_items, gqa::WARPS));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+        e0 = h->take_event();
+        e1 = h->take_event();
+        cudaEventRecord(e0, st);
+    }
+    gqa::attend_gqa_kernel<H><<<(unsigned)grid, gqa::WARPS * 32, smem, st>>>(a);
+    KIVI_LAUNCHED();
+    if (h->profile) {
+        cudaEventRecord(e1, st);
+        h->events.emplace_back(e0, e1);
+    }
+    h->main_launches++;
+    h->total_launches++;
+    gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
+        h->part_o, h->part_ml, (int)n_sub, H, out, weights ? h->stats : nullptr);
+    KIVI_LAUNCHED();
+    h->total_launches++;
+    if (weights) {
+        fast::normalize_weights_kernel<<<grid_for(U * H * h->l), 256, 0, st>>>(weights, h->stats,
+                                                                                h->l, U * H);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
@@ -700,6 +770,8 @@ kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float
     if (fast_ok && h->attend_path != 1) {
         const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
         const float qscale = scale * fast::LOG2E;
+        if (q_per_kv == 4) return launch_gqa<4>(h, t_q, out, weights, qscale, st);
+        if (q_per_kv == 2) return launch_gqa<2>(h, t_q, out, weights, qscale, st);
         if (h->cfg.bits == 2) return launch_fast<2>(h, t_q, out, weights, qscale, st);
         return launch_fast<4>(h, t_q, out, weights, qscale, st);
     }

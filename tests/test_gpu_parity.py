@@ -246,23 +246,52 @@ def test_fast_equals_generic_closely(cuda):
         assert rel_l2(oa[u], ob[u]) <= 1e-5
 
 
-def test_gqa_generic_matches_per_head_reference(cuda):
-    # GQA: one append, q_per_kv query heads (reference emulates with copies)
+def run_gqa(cfg, U, qpk, l0, steps, path, seed, weights=False):
+    """GQA: one append per unit, q_per_kv query heads; the reference emulates
+    each head with its own state copy."""
     ck = checker()
-    rng = np.random.default_rng(9)
-    cfg = (2, 32, 128, 128)
-    U, qpk, l0 = 2, 4, 300
-    K, V = rnd(rng, U, l0, 128), rnd(rng, U, l0, 128)
+    rng = np.random.default_rng(seed)
+    bits, G, R, d = cfg
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
     cache = kb.KVCache(kb.CacheConfig(*cfg), U)
+    cache.set_attend_path(path)
     cache.prefill(dev(K), dev(V))
-    q, tk, tv = rnd(rng, U, qpk, 128), rnd(rng, U, 128), rnd(rng, U, 128)
-    out = cache.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk).cpu().numpy()
+    refs = [[ck.unit(*cfg) for _ in range(qpk)] for _ in range(U)]
     for u in range(U):
         for h in range(qpk):
-            r = ck.unit(*cfg)
-            r.prefill(K[u], V[u])
-            ro = r.decode(q[u, h], tk[u], tv[u])
-            assert rel_l2(out[u, h], ro) <= 1e-6
+            refs[u][h].prefill(K[u], V[u])
+    worst, worst_w = 0.0, 0.0
+    for _ in range(steps):
+        q, tk, tv = rnd(rng, U, qpk, d), rnd(rng, U, d), rnd(rng, U, d)
+        res = cache.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk, weights=weights)
+        out, w = res if weights else (res, None)
+        out = out.cpu().numpy()
+        for u in range(U):
+            for h in range(qpk):
+                ro, rw = refs[u][h].decode(q[u, h], tk[u], tv[u], weights=True)
+                worst = max(worst, rel_l2(out[u, h], ro))
+                if weights:
+                    worst_w = max(worst_w, float(np.max(np.abs(w[u, h].cpu().numpy() - rw))))
+    return worst, worst_w
+
+
+def test_gqa_generic_matches_per_head_reference(cuda):
+    e, _ = run_gqa((2, 32, 128, 128), U=2, qpk=4, l0=300, steps=2, path="generic", seed=9)
+    assert e <= 1e-6, e
+
+
+@pytest.mark.parametrize("qpk", [2, 4])
+@pytest.mark.parametrize("l0", [1, 100, 255, 256, 300, 777])
+def test_gqa_fast_vs_reference(cuda, qpk, l0):
+    e, ew = run_gqa((2, 32, 128, 128), U=3, qpk=qpk, l0=l0, steps=3, path="fast", seed=l0 + qpk,
+                    weights=True)
+    assert e <= 1e-5, e
+    assert ew <= 1e-5, ew
+
+
+def test_gqa_fast_across_flush(cuda):
+    e, _ = run_gqa((2, 32, 128, 128), U=2, qpk=4, l0=2000, steps=130, path="fast", seed=77)
+    assert e <= 1e-5, e
 
 
 def test_single_token_exact(cuda):
