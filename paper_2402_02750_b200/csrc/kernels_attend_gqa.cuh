@@ -28,11 +28,17 @@ using fast::SLOT;
 using fast::SUB;
 constexpr int WARPS = 4;
 
+// q table row stride: 2H + 2 floats.  A key-tile step reads 16 distinct
+// channels c (c mod 16 all different); with stride 2H+2 (10 or 6 floats) the
+// 64-bit loads of those rows cover 32 distinct banks.
+template <int H>
+constexpr int QT_STRIDE = 2 * H + 2;
+
 template <int H>
 struct GS {  // per-warp shared memory
     static constexpr int QRAW_OFF = 2 * SLOT;                 // [H][128] staged q rows
-    static constexpr int QT_OFF = QRAW_OFF + H * D * 4;        // [128][2H]: qs_h, qk_h
-    static constexpr int PROBS_OFF = QT_OFF + D * 2 * H * 4;   // [256][H]
+    static constexpr int QT_OFF = QRAW_OFF + H * D * 4;        // [128][QT_STRIDE]: qs_h, qk_h
+    static constexpr int PROBS_OFF = QT_OFF + D * QT_STRIDE<H> * 4;  // [256][H]
     static constexpr int BAR_OFF = PROBS_OFF + SUB * H * 4;
     static constexpr int BYTES = BAR_OFF + 16;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
@@ -123,7 +129,7 @@ __device__ __forceinline__ void kq_tiles_heads(uint8_t* slot, const float* qt, f
             const int c = sl * 32 + ((i + rot) & 31);
             const uint32_t w = *reinterpret_cast<const uint32_t*>(codes + c * 8 + hf * 4);
             const float2 pr = *reinterpret_cast<const float2*>(pairs + c * 8);
-            const float* q = qt + c * 2 * H;
+            const float* q = qt + c * QT_STRIDE<H>;
             float2 M[H / 2];
             const float diff = pr.y - pr.x;
 #pragma unroll
@@ -158,7 +164,9 @@ __device__ __forceinline__ void kq_tiles_heads(uint8_t* slot, const float* qt, f
     if (tl < ntiles) {
         const int row0 = lane & ~3;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk0 = 0; kk0 < 4; ++kk0) {
+            // lane-dependent order: the 8 lanes of a load phase hit 8 slots
+            const int kk = kk0 ^ (sl >> 1) ^ (hf << 1);
             const int k = 4 * sl + kk;  // token within the half
             float v[H];
 #pragma unroll
@@ -199,7 +207,7 @@ __device__ __forceinline__ void kf_rows_heads(const uint8_t* slot, const float* 
     for (int h = 0; h < H; ++h) {
         float qv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) qv[i] = qt[(4 * lane + i) * 2 * H + h];
+        for (int i = 0; i < 4; ++i) qv[i] = qt[(4 * lane + i) * QT_STRIDE<H> + h];
         float part[F_ROWS];
 #pragma unroll
         for (int r = 0; r < F_ROWS; ++r) {
@@ -417,8 +425,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArg
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const float qs = v[i] * a.qscale;
-                        qt[(4 * lane + i) * 2 * H + h] = qs;
-                        qt[(4 * lane + i) * 2 * H + H + h] = qs * ksc;
+                        qt[(4 * lane + i) * QT_STRIDE<H> + h] = qs;
+                        qt[(4 * lane + i) * QT_STRIDE<H> + H + h] = qs * ksc;
                     }
                 }
                 __syncwarp();
