@@ -358,6 +358,18 @@ __device__ __forceinline__ void v_finalize_heads(uint8_t* slot, const float2* va
         if (lane == h) part_ml[h] = ml[h];
 }
 
+// Item order: sub-chunk-major with the LAST sub-chunk first.  Item i -> unit
+// i mod U, sub-chunk n_per_unit-1 - i/U.  The heavy items (the ones holding
+// fp32 residual rows) are then the first U items and spread over U warps; in
+// unit-major order with a static stride they all landed on the few warps
+// whose index is = n_per_unit-1 (mod n_per_unit) and idled 31 % of the SMs.
+__device__ __forceinline__ fast::ItemPlan plan_gqa(const fast::FastArgs& a, int i) {
+    const int nu = a.n_items / a.n_per_unit;
+    const int kk = i / nu;
+    const int u = i - kk * nu;
+    return fast::plan_item<2>(a, u * a.n_per_unit + (a.n_per_unit - 1 - kk));
+}
+
 template <int H>
 __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArgs a) {
     using WS = GS<H>;
@@ -381,7 +393,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArg
 
     int f_item = gw, f_job = 0;
     fast::ItemPlan f_plan{};
-    if (f_item < a.n_items) f_plan = fast::plan_item<2>(a, f_item);
+    if (f_item < a.n_items) f_plan = plan_gqa(a, f_item);
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArg
         if (++f_job == f_plan.njobs) {
             f_item += tw;
             f_job = 0;
-            if (f_item < a.n_items) f_plan = fast::plan_item<2>(a, f_item);
+            if (f_item < a.n_items) f_plan = plan_gqa(a, f_item);
         }
     };
     issue_next(0);
@@ -412,7 +424,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArg
     };
 
     for (int item = gw; item < a.n_items; item += tw) {
-        const fast::ItemPlan p = fast::plan_item<2>(a, item);
+        const fast::ItemPlan p = plan_gqa(a, item);
         const int nk = p.nkq + p.nkf;
         for (int j = 0; j < nk; ++j) {
             uint8_t* slot = wait_slot();

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "kernels_attend_fast.cuh"
 #include "kernels_attend_gqa.cuh"
+#include "kernels_attend_gqa_tc.cuh"
 #include "kernels_attend_generic.cuh"
 #include "kernels_quant.cuh"
 
@@ -417,10 +418,14 @@ template <int H>
 kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                        cudaStream_t st) {
     using WS = gqa::GS<H>;
+    using TWS = gqa_tc::TS<H>;
     const int64_t U = h->n_units;
     if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "GQA attend path: cache too large for 32-bit indexing");
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
+    // tensor-core body = whole 256-token sub-chunks below floor32(vg)
+    static const int use_tc = env_int("KIVI_GQA_TC", 1);
+    const int64_t nfull = use_tc ? ((h->vg() / 32) * 32) / fast::SUB : 0;
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * H * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub * H);
@@ -433,40 +438,77 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     a.kg = (int)h->kg();
     a.vg = (int)h->vg();
     a.n_sub = (int)n_sub;
-    a.k_first = 0;
-    a.n_per_unit = (int)n_sub;
-    a.n_items = (int)(U * n_sub);
     a.q = q;
     a.qscale = qscale;
     a.part_o = h->part_o;
     a.part_ml = h->part_ml;
     a.wlog = weights;
     const int smem = WS::STRIDE * gqa::WARPS;
+    const int smem_tc = TWS::STRIDE * gqa_tc::WARPS;
     const int key = 4 + H;
     if (h->fast_per_sm[key][2] == 0) {
         KIVI_CUDA(cudaFuncSetAttribute(gqa::attend_gqa_kernel<H>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        KIVI_CUDA(cudaFuncSetAttribute(gqa_tc::attend_gqa_tc_kernel<H>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, gqa::attend_gqa_kernel<H>, gqa::WARPS * 32, smem));
         h->fast_per_sm[key][2] = per_sm < 1 ? 1 : per_sm;
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, gqa_tc::attend_gqa_tc_kernel<H>, gqa_tc::WARPS * 32, smem_tc));
+        h->fast_per_sm[key][3] = per_sm < 1 ? 1 : per_sm;
     }
-    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][2],
-                                           ceil_div(a.n_items, gqa::WARPS));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->profile) {
         e0 = h->take_event();
         e1 = h->take_event();
         cudaEventRecord(e0, st);
     }
-    gqa::attend_gqa_kernel<H><<<(unsigned)grid, gqa::WARPS * 32, smem, st>>>(a);
-    KIVI_LAUNCHED();
+    if (!h->side) {
+        KIVI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        KIVI_CUDA(dalloc(&h->work, 1));
+    }
+    const bool has_tail = n_sub > nfull;
+    static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 1);
+    cudaStream_t tail_st = nfull > 0 ? h->side : st;
+    if (has_tail) {
+        // items holding fp32 residual rows: CUDA-core kernel, concurrently
+        if (tail_st != st) {
+            KIVI_CUDA(cudaEventRecord(h->ev_fork, st));
+            KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        }
+        a.k_first = (int)nfull;
+        a.n_per_unit = (int)(n_sub - nfull);
+        a.n_items = (int)(U * a.n_per_unit);
+        const int per_sm = tail_st != st ? tail_ctas : h->fast_per_sm[key][2];
+        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
+                                               ceil_div(a.n_items, gqa::WARPS));
+        gqa::attend_gqa_kernel<H><<<(unsigned)grid, gqa::WARPS * 32, smem, tail_st>>>(a);
+        KIVI_LAUNCHED();
+        if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
+        h->total_launches++;
+    }
+    if (nfull > 0) {
+        a.k_first = 0;
+        a.n_per_unit = (int)nfull;
+        a.n_items = (int)(U * nfull);
+        a.work = h->work;
+        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int), st));
+        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][3],
+                                               ceil_div(a.n_items, gqa_tc::WARPS));
+        gqa_tc::attend_gqa_tc_kernel<H><<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    if (has_tail && tail_st != st) KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
     if (h->profile) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
     }
     h->main_launches++;
-    h->total_launches++;
     gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
         h->part_o, h->part_ml, (int)n_sub, H, out, weights ? h->stats : nullptr);
     KIVI_LAUNCHED();

@@ -246,13 +246,18 @@ def test_fast_equals_generic_closely(cuda):
         assert rel_l2(oa[u], ob[u]) <= 1e-5
 
 
-def run_gqa(cfg, U, qpk, l0, steps, path, seed, weights=False):
+def run_gqa(cfg, U, qpk, l0, steps, path, seed, weights=False, kscale=1.0, vscale=1.0,
+            qscale=1.0, outliers=()):
     """GQA: one append per unit, q_per_kv query heads; the reference emulates
-    each head with its own state copy."""
+    each head with its own state copy.  kscale/vscale/qscale and
+    key outlier channels (x50, analysis.hpp:59-61) move the operand ranges the
+    tensor-core path rescales per job."""
     ck = checker()
     rng = np.random.default_rng(seed)
     bits, G, R, d = cfg
-    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    K, V = rnd(rng, U, l0, d, scale=kscale), rnd(rng, U, l0, d, scale=vscale)
+    for c in outliers:
+        K[:, :, c] *= 50.0
     cache = kb.KVCache(kb.CacheConfig(*cfg), U)
     cache.set_attend_path(path)
     cache.prefill(dev(K), dev(V))
@@ -262,7 +267,10 @@ def run_gqa(cfg, U, qpk, l0, steps, path, seed, weights=False):
             refs[u][h].prefill(K[u], V[u])
     worst, worst_w = 0.0, 0.0
     for _ in range(steps):
-        q, tk, tv = rnd(rng, U, qpk, d), rnd(rng, U, d), rnd(rng, U, d)
+        q = rnd(rng, U, qpk, d, scale=qscale)
+        tk, tv = rnd(rng, U, d, scale=kscale), rnd(rng, U, d, scale=vscale)
+        for c in outliers:
+            tk[:, c] *= 50.0
         res = cache.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk, weights=weights)
         out, w = res if weights else (res, None)
         out = out.cpu().numpy()
@@ -287,6 +295,25 @@ def test_gqa_fast_vs_reference(cuda, qpk, l0):
                     weights=True)
     assert e <= 1e-5, e
     assert ew <= 1e-5, ew
+
+
+# (kscale, vscale, qscale, key outlier channels, tolerance).  The last case
+# has log2-domain logits of magnitude ~500: one fp32 ulp there is 3e-5, so
+# even the reference's own float cast of its double logits (attention.cpp:59-62)
+# moves the softmax by that much; the bar scales with the logit magnitude.
+@pytest.mark.parametrize("qpk", [2, 4])
+@pytest.mark.parametrize("scales", [(1e-3, 1e-3, 1.0, (), 1e-5), (30.0, 200.0, 3.0, (), 1e-5),
+                                    (1.0, 1.0, 1.0, (1, 17, 40), 1e-5),
+                                    (4.0, 0.01, 20.0, (5,), 5e-5)])
+def test_gqa_fast_operand_ranges(cuda, qpk, scales):
+    # the tensor-core body path scales its fp16 operands by 2^E per job and
+    # must keep fp32-class accuracy on 50x outlier key channels
+    ks, vs, qs, outl, tol = scales
+    e, ew = run_gqa((2, 32, 128, 128), U=3, qpk=qpk, l0=1100, steps=2, path="fast",
+                    seed=int(ks * 10 + vs) + qpk, weights=True, kscale=ks, vscale=vs, qscale=qs,
+                    outliers=outl)
+    assert e <= tol, e
+    assert ew <= tol, ew
 
 
 def test_gqa_fast_across_flush(cuda):
