@@ -283,7 +283,7 @@ __device__ __forceinline__ float2 softmax_item(float* probs, int ntok, float* wl
     __syncwarp();
     float mx = -INFINITY;
     for (int i = lane; i < ntok; i += 32) mx = fmaxf(mx, probs[i]);
-    mx = warp_max(mx);
+    mx = warp_max_redux(mx);
     float sm = 0.f;
     for (int i = lane; i < ntok; i += 32) {
         const float lg = probs[i];
@@ -673,8 +673,11 @@ __device__ __forceinline__ void issue_job(const FastArgs& a, int u, const JobDes
 
 // Any mix of quantized / fp32 keys and values per item (the residual window
 // and the last partial sub-chunk), any l.
-template <int B>
-__global__ void __launch_bounds__(WARPS * 32, 3) attend_tail_kernel(FastArgs a) {
+// NW warps per CTA: 4 when the tail runs alone; 1 when it runs beside the
+// body kernel on a side stream, so its CTAs fit in the shared memory the
+// body CTAs leave free and every tail item gets its own warp.
+template <int B, int NW = WARPS>
+__global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     using PB = P<B>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -690,8 +693,8 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_tail_kernel(FastArgs a) 
     }
     __syncwarp();
     const uint64_t policy = make_evict_first_policy();
-    const int gw = blockIdx.x * WARPS + warp;
-    const int tw = gridDim.x * WARPS;
+    const int gw = blockIdx.x * NW + warp;
+    const int tw = gridDim.x * NW;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
 
     int f_item = gw, f_job = 0;

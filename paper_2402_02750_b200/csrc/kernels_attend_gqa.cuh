@@ -370,8 +370,11 @@ __device__ __forceinline__ fast::ItemPlan plan_gqa(const fast::FastArgs& a, int 
     return fast::plan_item<2>(a, u * a.n_per_unit + (a.n_per_unit - 1 - kk));
 }
 
-template <int H>
-__global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArgs a) {
+// NW warps per CTA: 4 when this kernel runs every item; 1 when it runs only
+// the residual-window items beside the tensor-core body kernel, so its
+// shared memory leaves room for two body CTAs on the same SM.
+template <int H, int NW = WARPS>
+__global__ void __launch_bounds__(NW * 32, 2) attend_gqa_kernel(fast::FastArgs a) {
     using WS = GS<H>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -387,8 +390,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_kernel(fast::FastArg
     }
     __syncwarp();
     const uint64_t policy = make_evict_first_policy();
-    const int gw = blockIdx.x * WARPS + warp;
-    const int tw = gridDim.x * WARPS;
+    const int gw = blockIdx.x * NW + warp;
+    const int tw = gridDim.x * NW;
     const float ksc = fast::TWO_POW_64 / 3.0f;
 
     int f_item = gw, f_job = 0;

@@ -51,26 +51,52 @@ namespace kivi_b200 {
 namespace gqa_tc {
 
 using fast::D;
-using fast::SLOT;
+// Job geometry: a key job is KT 32-token tiles (KT KB codes + KT KB (lo, hi)),
+// a value job VT tokens (VT x 32 B codes + VT x 32 B pairs).  Small jobs keep
+// the per-warp shared memory at ~19 KB, so 3 CTAs x 4 warps fit an SM: the
+// kernel is latency-bound and needs the warps more than the larger jobs.
+#ifndef KIVI_GQA_TC_KT
+#define KIVI_GQA_TC_KT 2
+#endif
+constexpr int KT = KIVI_GQA_TC_KT;
+constexpr int VT = KT * 32;
+constexpr int SLOT = KT * 2048;
 using fast::SUB;
-constexpr int WARPS = 4;
+#ifndef KIVI_GQA_TC_WARPS
+#define KIVI_GQA_TC_WARPS 4
+#endif
+constexpr int WARPS = KIVI_GQA_TC_WARPS;   // warps per CTA
+constexpr int MIN_CTAS = KT == 2 ? 3 : 2;
 constexpr int BFK_ROW = 9;        // uint2 per consumer lane in the key B buffer (8 K steps + pad)
 constexpr int BFV_CG = 72;        // 32-bit words per channel group in the value B buffer (64 + pad)
 constexpr int BIAS_ROW = 17;      // floats per lane row of the key-bias transpose
 constexpr uint32_t FULL = 0xffffffffu;
 
+// probs layout: token pairs (t, t+4) with t & 4 == 0 side by side per head,
+// so the value producer reads (p_h[t], p_h[t+4]) as one float2:
+//   pidx(t, h) = ((t >> 3) * 4 + (t & 3)) * 2H + 2h + ((t >> 2) & 1)
+template <int H>
+__device__ __forceinline__ int pidx(int t, int h) {
+    return ((t >> 3) * 4 + (t & 3)) * (2 * H) + 2 * h + ((t >> 2) & 1);
+}
+
 template <int H>
 struct TS {  // per-warp shared memory
-    static constexpr int QRAW_OFF = 2 * SLOT;                  // [H][128] staged q rows
-    static constexpr int PROBS_OFF = QRAW_OFF + H * D * 4;     // [256][H] logits -> p
+    // q rows are staged (TMA) into the key-bias scratch: q is consumed at the
+    // start of an item, the scratch only afterwards, and the next item's q
+    // is issued only after this item's key jobs are done.
+    static constexpr int QB_OFF = 2 * SLOT;                   // [H][128] q | [32][17] bias
+    static constexpr int QB_BYTES = (32 * BIAS_ROW * 4 > H * D * 4) ? 32 * BIAS_ROW * 4 : H * D * 4;
+    static constexpr int PROBS_OFF = QB_OFF + ((QB_BYTES + 15) & ~15);  // [256 x H] p (pidx)
     static constexpr int BF_OFF = PROBS_OFF + SUB * H * 4;     // B fragments (keys | values)
-    static constexpr int BF_BYTES = 32 * BFK_ROW * 8;          // 2304 = 2 x 4 x 72 x 4
-    static constexpr int BIAS_OFF = BF_OFF + BF_BYTES;         // [32][17] key-bias partials
-    static constexpr int ZS_OFF = BIAS_OFF + 32 * BIAS_ROW * 4;  // [H][4] value z sums
+    static constexpr int BFK_BYTES = 32 * BFK_ROW * 8;         // 2304 = 2 x 4 x 72 x 4
+    static constexpr int BF_BYTES = 2 * BFK_BYTES;            // double-buffered
+    static constexpr int ZS_OFF = BF_OFF + BF_BYTES;           // [H][4] value z sums
     static constexpr int BAR_OFF = ZS_OFF + 16 * 4;
     static constexpr int BYTES = BAR_OFF + 16;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
     static_assert(2 * 4 * BFV_CG * 4 <= BF_BYTES, "value B buffers overflow");
+    static_assert(BFK_BYTES % 16 == 0, "key B buffer alignment");
 };
 
 __device__ __forceinline__ void mma_f16(float4& d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -81,12 +107,15 @@ __device__ __forceinline__ void mma_f16(float4& d, uint32_t a0, uint32_t a1, uin
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// (x0, x1) -> fp16x2 words (hi, lo) with x = hi + lo to ~2^-21 relative.
-__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& whi, uint32_t& wlo) {
-    const float h0 = __uint_as_float(__float_as_uint(x0) & 0xFFFFE000u);
-    const float h1 = __uint_as_float(__float_as_uint(x1) & 0xFFFFE000u);
-    __half2 hh = __floats2half2_rn(h0, h1);
-    __half2 ll = __floats2half2_rn(x0 - h0, x1 - h1);
+// x = (x0, x1) -> fp16x2 words (hi, lo) with x = hi + lo to ~2^-21 relative:
+// hi = x truncated to 10 mantissa bits (exact in fp16), lo = x - hi (exact in
+// fp32, one packed FFMA2), rounded to fp16.
+__device__ __forceinline__ void split_pair(float2 x, uint32_t& whi, uint32_t& wlo) {
+    const float2 h = make_float2(__uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                 __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+    const float2 l = __ffma2_rn(h, make_float2(-1.0f, -1.0f), x);
+    __half2 hh = __floats2half2_rn(h.x, h.y);
+    __half2 ll = __floats2half2_rn(l.x, l.y);
     whi = *reinterpret_cast<uint32_t*>(&hh);
     wlo = *reinterpret_cast<uint32_t*>(&ll);
 }
@@ -122,21 +151,38 @@ __device__ __forceinline__ CodeQuad code_quad(uint32_t x) {
     return q;
 }
 
+// Two MMAs sharing B in one asm statement: the eight A registers are live at
+// once, so ptxas gives them distinct quads (with one MMA per statement it
+// funnelled every MMA through the same four registers, serialising the
+// extraction LOP3s behind the previous MMA's operand read).
+__device__ __forceinline__ void mma_f16_x2(float4& d0, float4& d1, const CodeQuad& ca,
+                                           const CodeQuad& cb, uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%8,%9,%10,%11}, "
+        "{%16,%17}, {%0,%1,%2,%3};\n\t"
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%4,%5,%6,%7}, {%12,%13,%14,%15}, "
+        "{%16,%17}, {%4,%5,%6,%7};"
+        : "+f"(d0.x), "+f"(d0.y), "+f"(d0.z), "+f"(d0.w), "+f"(d1.x), "+f"(d1.y), "+f"(d1.z),
+          "+f"(d1.w)
+        : "r"(ca.c[0]), "r"(ca.c[1]), "r"(cb.c[0]), "r"(cb.c[1]), "r"(ca.c[2]), "r"(ca.c[3]),
+          "r"(cb.c[2]), "r"(cb.c[3]), "r"(b0), "r"(b1));
+}
+
+
 // -------------------------------------------------------------------------
-// One key job: 4 tiles (codes [4][1024 B], pairs [4][128] (lo, hi)) -> the
-// log2-domain logits of 128 tokens x H heads at probs_dst[token * H + h].
+// One key job: KT tiles (codes [KT][1024 B], pairs [KT][128] (lo, hi)) -> the
+// log2-domain logits of tokens tok0 .. tok0+32KT-1 x H heads at probs[pidx].
 // -------------------------------------------------------------------------
 template <int H>
-__device__ __forceinline__ void key_job(const uint8_t* slot, const float (&qv)[H][4], float qmax,
-                                        float* probs_dst, uint8_t* bf, float* biasm, int lane,
+__device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[H][2], float qmax,
+                                        float* probs, int tok0, uint8_t* bf, float* biasm, int lane,
                                         uint32_t sel) {
     const int g = lane >> 2, t = lane & 3;
-    const float4* pairs4 = reinterpret_cast<const float4*>(slot + 4 * 1024);
-    // pre-pass over this lane's channels 4L..4L+3 of the 4 tiles: spans,
+    const float4* pairs4 = reinterpret_cast<const float4*>(slot + KT * 1024);
+    // pre-pass over this lane's channels 4L..4L+3 of the KT tiles: spans,
     // bias partials, job-wide span maximum
     float dmax = 0.f;
 #pragma unroll
-    for (int T = 0; T < 4; ++T) {
+    for (int T = 0; T < KT; ++T) {
         const float4 p01 = pairs4[T * 64 + 2 * lane];
         const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
         const float lo[4] = {p01.x, p01.z, p23.x, p23.z};
@@ -144,44 +190,50 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float (&qv)[H
                                  fmaxf(p23.y - p23.x, p23.w - p23.z)));
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            float b = qv[h][0] * lo[0];
-            b = fmaf(qv[h][1], lo[1], b);
-            b = fmaf(qv[h][2], lo[2], b);
-            b = fmaf(qv[h][3], lo[3], b);
+            float b = qv[h][0].x * lo[0];
+            b = fmaf(qv[h][0].y, lo[1], b);
+            b = fmaf(qv[h][1].x, lo[2], b);
+            b = fmaf(qv[h][1].y, lo[3], b);
             biasm[lane * BIAS_ROW + T * H + h] = b;
         }
     }
-    dmax = warp_max(dmax);
+    dmax = warp_max_redux(dmax);
     const int eb = exp_byte(qmax * dmax * (1.0f / 3.0f));
     const float f = scale_up(eb) * (1.0f / 3.0f);
     __syncwarp();
     // bias column sums: lane L sums column L & 15 over 16 rows, then xor 16
     float bs = 0.f;
     {
-        const int col = lane & 15, r0 = (lane >> 4) * 16;
+        // KT * H <= 16 columns; lane L sums column L % NC over rows of its share
+        constexpr int NC = (KT * H <= 8) ? 8 : 16;
+        constexpr int RPL = NC;  // rows per lane
+        const int col = lane & (NC - 1), r0 = (lane / NC) * RPL;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) bs += biasm[(r0 + r) * BIAS_ROW + col];
-        bs += __shfl_xor_sync(FULL, bs, 16);
+        for (int r = 0; r < RPL; ++r) bs += biasm[(r0 + r) * BIAS_ROW + col];
+#pragma unroll
+        for (int o = NC; o < 32; o <<= 1) bs += __shfl_xor_sync(FULL, bs, o);
     }
-    uint2* bfk = reinterpret_cast<uint2*>(bf);
     const int s_p = lane >> 2, t_p = lane & 3;  // producer -> consumer K step / lane slot
-#pragma unroll 1
-    for (int T = 0; T < 4; ++T) {
-        // ---- producer: B fragments of tile T ----
+    // producer: B fragments of tile T into buffer T & 1
+    auto produce = [&](int T) {
+        uint2* bfk = reinterpret_cast<uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
         const float4 p01 = pairs4[T * 64 + 2 * lane];
         const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
-        const float d0 = (p01.y - p01.x) * f, d1 = (p01.w - p01.z) * f;
-        const float d2 = (p23.y - p23.x) * f, d3 = (p23.w - p23.z) * f;
+        const float2 f2 = make_float2(f, f);
+        const float2 d01 = __fmul2_rn(make_float2(p01.y - p01.x, p01.w - p01.z), f2);
+        const float2 d23 = __fmul2_rn(make_float2(p23.y - p23.x, p23.w - p23.z), f2);
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             uint32_t hi01, lo01, hi23, lo23;
-            split_pair(qv[h][0] * d0, qv[h][1] * d1, hi01, lo01);
-            split_pair(qv[h][2] * d2, qv[h][3] * d3, hi23, lo23);
+            split_pair(__fmul2_rn(qv[h][0], d01), hi01, lo01);
+            split_pair(__fmul2_rn(qv[h][1], d23), hi23, lo23);
             bfk[((2 * h) * 4 + t_p) * BFK_ROW + s_p] = make_uint2(hi01, hi23);
             bfk[((2 * h + 1) * 4 + t_p) * BFK_ROW + s_p] = make_uint2(lo01, lo23);
         }
-        __syncwarp();
-        // ---- consumer: 8 K steps x 2 MMAs ----
+    };
+    // consumer: 8 K steps x 2 MMAs of tile T, then its logits
+    auto consume = [&](int T) {
+        const uint2* bfk = reinterpret_cast<const uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
         float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
         const uint8_t* ct = slot + T * 1024 + 4 * (g >> 2);
 #pragma unroll
@@ -195,66 +247,84 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float (&qv)[H
             const CodeQuad c23 = code_quad(__byte_perm(w2, w3, sel));
             uint2 b = make_uint2(0u, 0u);
             if (g < 2 * H) b = bfk[lane * BFK_ROW + s];
-            mma_f16(acc0, c01.c[0], c01.c[1], c23.c[0], c23.c[1], b.x, b.y);
-            mma_f16(acc1, c01.c[2], c01.c[3], c23.c[2], c23.c[3], b.x, b.y);
+            mma_f16_x2(acc0, acc1, c01, c23, b.x, b.y);
         }
-        const float bias = __shfl_sync(FULL, bs, (T * H + t) & 15);
-        __syncwarp();  // the next tile's producer overwrites bfk
+        const float bias = __shfl_sync(FULL, bs, (T * H + t) & 15);  // column T*H+t
         if (t < H) {
-            float* dst = probs_dst + (T * 32 + 4 * g) * H + t;
-            dst[0 * H] = fmaf(acc0.x + acc0.y, unscale(eb, code_pos(0)), bias);
-            dst[1 * H] = fmaf(acc0.z + acc0.w, unscale(eb, code_pos(1)), bias);
-            dst[2 * H] = fmaf(acc1.x + acc1.y, unscale(eb, code_pos(2)), bias);
-            dst[3 * H] = fmaf(acc1.z + acc1.w, unscale(eb, code_pos(3)), bias);
+            // tokens tb + j, j = 0..3 share the pair block of tb (tb & 3 == 0)
+            const int tb = tok0 + T * 32 + 4 * g;
+            float* dst = probs + pidx<H>(tb, t);
+            dst[0 * 2 * H] = fmaf(acc0.x + acc0.y, unscale(eb, code_pos(0)), bias);
+            dst[1 * 2 * H] = fmaf(acc0.z + acc0.w, unscale(eb, code_pos(1)), bias);
+            dst[2 * 2 * H] = fmaf(acc1.x + acc1.y, unscale(eb, code_pos(2)), bias);
+            dst[3 * 2 * H] = fmaf(acc1.z + acc1.w, unscale(eb, code_pos(3)), bias);
         }
+    };
+    // two fragment buffers: one warp barrier per tile orders producer and
+    // consumer (tile T+1's producer writes the buffer tile T-1 read before
+    // the barrier of tile T).  Building tile T+1 during tile T's MMAs measured
+    // slower (374 vs 360 us on C3): register pressure, no extra overlap.
+#pragma unroll 1
+    for (int T = 0; T < KT; ++T) {
+        produce(T);
+        __syncwarp();
+        consume(T);
     }
+    __syncwarp();  // the next job's producer overwrites the buffers
 }
 
-// Softmax of each head over the item's 256 tokens (probs [token][H], in
-// place, log2 domain) -> p in (0, 1]; ml[h] = (max, sum).
+// Softmax of each head over the item's 256 tokens (probs in pidx layout, in
+// place, log2 domain) -> p in (0, 1]; ml[h] = (max, sum).  Lane L owns the
+// pair blocks L + 32i (tokens tb, tb+4 with tb = (b >> 2) * 8 + (b & 3)).
 template <int H>
 __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t wstride, float2* ml,
                                               int lane) {
     __syncwarp();
-    float v[8][H];
+    float2 v[4][H];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float* src = probs + (lane + 32 * i) * H;
-        if constexpr (H == 4) {
-            const float4 x = *reinterpret_cast<const float4*>(src);
-            v[i][0] = x.x; v[i][1] = x.y; v[i][2] = x.z; v[i][3] = x.w;
-        } else {
-            const float2 x = *reinterpret_cast<const float2*>(src);
-            v[i][0] = x.x; v[i][1] = x.y;
+    for (int i = 0; i < 4; ++i) {
+        const float4* src = reinterpret_cast<const float4*>(probs + (lane + 32 * i) * 2 * H);
+#pragma unroll
+        for (int h2 = 0; h2 < H / 2; ++h2) {
+            const float4 x = src[h2];
+            v[i][2 * h2] = make_float2(x.x, x.y);
+            v[i][2 * h2 + 1] = make_float2(x.z, x.w);
         }
     }
     float m[H], sm[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-        m[h] = v[0][h];
+        m[h] = fmaxf(v[0][h].x, v[0][h].y);
 #pragma unroll
-        for (int i = 1; i < 8; ++i) m[h] = fmaxf(m[h], v[i][h]);
-        m[h] = warp_max(m[h]);
+        for (int i = 1; i < 4; ++i) m[h] = fmaxf(m[h], fmaxf(v[i][h].x, v[i][h].y));
+        m[h] = warp_max_redux(m[h]);
         sm[h] = 0.f;
     }
     if (wlog) {
 #pragma unroll
-        for (int h = 0; h < H; ++h)
+        for (int i = 0; i < 4; ++i) {
+            const int b = lane + 32 * i;
+            const int tb = (b >> 2) * 8 + (b & 3);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) wlog[h * wstride + lane + 32 * i] = v[i][h];
+            for (int h = 0; h < H; ++h) {
+                wlog[h * wstride + tb] = v[i][h].x;
+                wlog[h * wstride + tb + 4] = v[i][h].y;
+            }
+        }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            v[i][h] = fast::ex2_approx(v[i][h] - m[h]);
-            sm[h] += v[i][h];
+            v[i][h].x = fast::ex2_approx(v[i][h].x - m[h]);
+            v[i][h].y = fast::ex2_approx(v[i][h].y - m[h]);
+            sm[h] += v[i][h].x + v[i][h].y;
         }
-        float* dst = probs + (lane + 32 * i) * H;
-        if constexpr (H == 4)
-            *reinterpret_cast<float4*>(dst) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
-        else
-            *reinterpret_cast<float2*>(dst) = make_float2(v[i][0], v[i][1]);
+        float4* dst = reinterpret_cast<float4*>(probs + (lane + 32 * i) * 2 * H);
+#pragma unroll
+        for (int h2 = 0; h2 < H / 2; ++h2)
+            dst[h2] = make_float4(v[i][2 * h2].x, v[i][2 * h2].y, v[i][2 * h2 + 1].x,
+                                  v[i][2 * h2 + 1].y);
     }
 #pragma unroll
     for (int h = 0; h < H; ++h) ml[h] = make_float2(m[h], warp_sum(sm[h]));
@@ -262,25 +332,25 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
 }
 
 // -------------------------------------------------------------------------
-// One value job: 128 tokens (codes [128][32 B], pairs [128][4] (lo, hi)),
-// probabilities p_src[token * H + h] -> vacc[cg][m], zs[h] (this lane's
-// share of sum_t p_h[t] z[t][cg = lane & 3]).  eb_run is the running
+// One value job: VT tokens (codes [VT][32 B], pairs [VT][4] (lo, hi)),
+// probabilities p_src (pidx layout, job-relative) -> vacc[cg][m], zs[h]
+// (this lane's share of sum_t p_h[t] z[t][cg = lane & 3], token pair halves).  eb_run is the running
 // exponent byte (the larger of all jobs so far: smaller 2^E).
 // -------------------------------------------------------------------------
 template <int H>
 __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_src, float4 (&vacc)[4][2],
-                                          float (&zs)[H], int& eb_run, bool first, uint8_t* bf,
+                                          float2 (&zs)[H], int& eb_run, bool first, uint8_t* bf,
                                           int lane, uint32_t sel) {
     const int g = lane >> 2, t = lane & 3;
-    const float4* pairs4 = reinterpret_cast<const float4*>(slot + 4096);
-    const float2* pairs2 = reinterpret_cast<const float2*>(slot + 4096);
+    const float4* pairs4 = reinterpret_cast<const float4*>(slot + VT * 32);
+    const float2* pairs2 = reinterpret_cast<const float2*>(slot + VT * 32);
     float dmax = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < VT / 16; ++i) {
         const float4 pr = pairs4[lane + 32 * i];
         dmax = fmaxf(dmax, fmaxf(pr.y - pr.x, pr.w - pr.z));
     }
-    dmax = warp_max(dmax);
+    dmax = warp_max_redux(dmax);
     const int eb = exp_byte(dmax * (1.0f / 3.0f));
     if (first) {
         eb_run = eb;
@@ -298,37 +368,32 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
     const int p = lane >> 2, cgp = lane & 3;
     const int tcons = p & 3, which = p >> 2;
     const int toff = (p < 4) ? p : p + 4;  // this producer's token pair: (toff, toff + 4)
-#pragma unroll 1
-    for (int s = 0; s < 8; ++s) {
+    // producer: B fragments of K step s into buffer s & 1
+    auto produce = [&](int s) {
         uint32_t* bv = reinterpret_cast<uint32_t*>(bf) + (s & 1) * (4 * BFV_CG);
-        // ---- producer: B fragments of K step s ----
-        {
-            const int ta = 16 * s + toff, tb = ta + 4;
-            const float2 pa = pairs2[ta * 4 + cgp], pb = pairs2[tb * 4 + cgp];
-            const float da = (pa.y - pa.x) * f, db = (pb.y - pb.x) * f;
-            float Pa[H], Pb[H];
-            if constexpr (H == 4) {
-                const float4 xa = *reinterpret_cast<const float4*>(p_src + ta * 4);
-                const float4 xb = *reinterpret_cast<const float4*>(p_src + tb * 4);
-                Pa[0] = xa.x; Pa[1] = xa.y; Pa[2] = xa.z; Pa[3] = xa.w;
-                Pb[0] = xb.x; Pb[1] = xb.y; Pb[2] = xb.z; Pb[3] = xb.w;
-            } else {
-                const float2 xa = *reinterpret_cast<const float2*>(p_src + ta * 2);
-                const float2 xb = *reinterpret_cast<const float2*>(p_src + tb * 2);
-                Pa[0] = xa.x; Pa[1] = xa.y;
-                Pb[0] = xb.x; Pb[1] = xb.y;
-            }
+        const int ta = 16 * s + toff, tb = ta + 4;
+        const float2 pa = pairs2[ta * 4 + cgp], pb = pairs2[tb * 4 + cgp];
+        const float2 d2 = __fmul2_rn(make_float2(pa.y - pa.x, pb.y - pb.x), make_float2(f, f));
+        const float2 z2 = make_float2(pa.x, pb.x);
+        const float4* pp = reinterpret_cast<const float4*>(p_src + pidx<H>(ta, 0));
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
+        for (int h2 = 0; h2 < H / 2; ++h2) {
+            const float4 x = pp[h2];  // (p_2h2[ta], p_2h2[tb], p_2h2+1[ta], p_2h2+1[tb])
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int h = 2 * h2 + e;
+                const float2 P = e ? make_float2(x.z, x.w) : make_float2(x.x, x.y);
                 uint32_t whi, wlo;
-                split_pair(Pa[h] * da, Pb[h] * db, whi, wlo);
-                zs[h] = fmaf(Pa[h], pa.x, fmaf(Pb[h], pb.x, zs[h]));
+                split_pair(__fmul2_rn(P, d2), whi, wlo);
+                zs[h] = __ffma2_rn(P, z2, zs[h]);
                 bv[cgp * BFV_CG + 2 * ((2 * h) * 4 + tcons) + which] = whi;
                 bv[cgp * BFV_CG + 2 * ((2 * h + 1) * 4 + tcons) + which] = wlo;
             }
         }
-        __syncwarp();
-        // ---- consumer: 4 channel groups x 2 MMAs ----
+    };
+    // consumer: 4 channel groups x 2 MMAs of K step s
+    auto consume = [&](int s) {
+        const uint32_t* bv = reinterpret_cast<const uint32_t*>(bf) + (s & 1) * (4 * BFV_CG);
 #pragma unroll
         for (int cg = 0; cg < 4; ++cg) {
             const uint8_t* cw = slot + 4 * (2 * cg + (g >> 2)) + (16 * s + t) * 32;
@@ -340,21 +405,29 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
             const CodeQuad c23 = code_quad(__byte_perm(w2, w3, sel));
             uint2 b = make_uint2(0u, 0u);
             if (g < 2 * H) b = reinterpret_cast<const uint2*>(bv + cg * BFV_CG)[lane];
-            mma_f16(vacc[cg][0], c01.c[0], c01.c[1], c23.c[0], c23.c[1], b.x, b.y);
-            mma_f16(vacc[cg][1], c01.c[2], c01.c[3], c23.c[2], c23.c[3], b.x, b.y);
+            mma_f16_x2(vacc[cg][0], vacc[cg][1], c01, c23, b.x, b.y);
         }
+    };
+    // one warp barrier per K step (two buffers, as in key_job)
+#pragma unroll 1
+    for (int s = 0; s < VT / 16; ++s) {
+        produce(s);
+        __syncwarp();
+        consume(s);
     }
 }
 
 // Write the item's H partials: lane (g, t) owns head t, channels
 // 32cg + 4g + {0..3}.
 template <int H>
-__device__ __forceinline__ void value_finalize(const float4 (&vacc)[4][2], float (&zs)[H], int eb,
-                                               const float2* ml, float* zsm, float* part_o,
+__device__ __forceinline__ void value_finalize(const float4 (&vacc)[4][2], const float2 (&zs2)[H],
+                                               int eb, const float2* ml, float* zsm, float* part_o,
                                                float2* part_ml, int lane) {
     const int g = lane >> 2, t = lane & 3;
+    float zs[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) {
+        zs[h] = zs2[h].x + zs2[h].y;
         zs[h] += __shfl_xor_sync(FULL, zs[h], 4);
         zs[h] += __shfl_xor_sync(FULL, zs[h], 8);
         zs[h] += __shfl_xor_sync(FULL, zs[h], 16);
@@ -390,17 +463,17 @@ __device__ __forceinline__ void value_finalize(const float4 (&vacc)[4][2], float
 // streamed through two TMA slots per warp (as fast::attend_body_kernel).
 // -------------------------------------------------------------------------
 template <int H>
-__global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_tc_kernel(fast::FastArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fast::FastArgs a) {
     using WS = TS<H>;
     using PB = fast::P<2>;
-    constexpr int NKJ = 2, NVJ = 2, NJ = 4;
+    constexpr int NKJ = (SUB / 32) / KT, NVJ = SUB / VT, NJ = NKJ + NVJ;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* wbase = smem_raw + warp * WS::STRIDE;
-    float* qraw = reinterpret_cast<float*>(wbase + WS::QRAW_OFF);
+    float* qraw = reinterpret_cast<float*>(wbase + WS::QB_OFF);
+    float* biasm = qraw;
     float* probs = reinterpret_cast<float*>(wbase + WS::PROBS_OFF);
     uint8_t* bf = wbase + WS::BF_OFF;
-    float* biasm = reinterpret_cast<float*>(wbase + WS::BIAS_OFF);
     float* zsm = reinterpret_cast<float*>(wbase + WS::ZS_OFF);
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WS::BAR_OFF);
     if (lane == 0) {
@@ -431,9 +504,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_tc_kernel(fast::Fast
             const int kk = a.k_first + f_k;
             fence_proxy_async_smem();
             if (f_job < NKJ) {
-                const int64_t tile0 = (int64_t)kk * (SUB / 32) + f_job * PB::KQ_TILES;
-                constexpr uint32_t cb = PB::KQ_TILES * PB::TILE_CODE;
-                constexpr uint32_t pb = PB::KQ_TILES * D * 8;
+                const int64_t tile0 = (int64_t)kk * (SUB / 32) + f_job * KT;
+                constexpr uint32_t cb = KT * PB::TILE_CODE;
+                constexpr uint32_t pb = KT * D * 8;
                 constexpr uint32_t qb = H * D * 4;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? qb : 0));
                 bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE, cb,
@@ -442,9 +515,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_tc_kernel(fast::Fast
                                      policy);
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * H * D, qb, bar);
             } else {
-                const int64_t ts = (int64_t)kk * SUB + (f_job - NKJ) * PB::VQ_TOK;
-                constexpr uint32_t cb = PB::VQ_TOK * PB::TOK_CODE;
-                constexpr uint32_t pb = PB::VQ_TOK * (D / fast::G) * 8;
+                const int64_t ts = (int64_t)kk * SUB + (f_job - NKJ) * VT;
+                constexpr uint32_t cb = VT * PB::TOK_CODE;
+                constexpr uint32_t pb = VT * (D / fast::G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
                 bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb, bar,
                                      policy);
@@ -480,25 +553,25 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_tc_kernel(fast::Fast
     for (int item = c_next; item < a.n_items; item = c_next) {
         const int u = item / nper;
         const int k = a.k_first + (item - u * nper);
-        float qv[H][4];
+        float2 qv[H][2];
         float qmax = 0.f;
 #pragma unroll 1
         for (int jk = 0; jk < NKJ; ++jk) {
             uint8_t* slot = wait_slot();
             if (jk == 0) {
+                const float2 qs2 = make_float2(a.qscale, a.qscale);
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
                     const float4 q4 = reinterpret_cast<const float4*>(qraw + h * D)[lane];
-                    qv[h][0] = q4.x * a.qscale;
-                    qv[h][1] = q4.y * a.qscale;
-                    qv[h][2] = q4.z * a.qscale;
-                    qv[h][3] = q4.w * a.qscale;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) qmax = fmaxf(qmax, fabsf(qv[h][i]));
+                    qv[h][0] = __fmul2_rn(make_float2(q4.x, q4.y), qs2);
+                    qv[h][1] = __fmul2_rn(make_float2(q4.z, q4.w), qs2);
+                    qmax = fmaxf(qmax, fmaxf(fmaxf(fabsf(qv[h][0].x), fabsf(qv[h][0].y)),
+                                             fmaxf(fabsf(qv[h][1].x), fabsf(qv[h][1].y))));
                 }
-                qmax = warp_max(qmax);
+                qmax = warp_max_redux(qmax);
+                __syncwarp();  // qraw is reused as the bias scratch below
             }
-            key_job<H>(slot, qv, qmax, probs + jk * 128 * H, bf, biasm, lane, sel);
+            key_job<H>(slot, qv, qmax, probs, jk * KT * 32, bf, biasm, lane, sel);
             release_slot();
         }
         float2 ml[H];
@@ -509,14 +582,14 @@ __global__ void __launch_bounds__(WARPS * 32, 2) attend_gqa_tc_kernel(fast::Fast
         for (int cg = 0; cg < 4; ++cg)
 #pragma unroll
             for (int m = 0; m < 2; ++m) vacc[cg][m] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float zs[H];
+        float2 zs[H];
 #pragma unroll
-        for (int h = 0; h < H; ++h) zs[h] = 0.f;
+        for (int h = 0; h < H; ++h) zs[h] = make_float2(0.f, 0.f);
         int eb_run = 0;
 #pragma unroll 1
         for (int jv = 0; jv < NVJ; ++jv) {
             uint8_t* slot = wait_slot();
-            value_job<H>(slot, probs + jv * 128 * H, vacc, zs, eb_run, jv == 0, bf, lane, sel);
+            value_job<H>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane, sel);
             if (jv == NVJ - 1) {
                 const int64_t pi = ((int64_t)u * a.n_sub + k) * H;
                 value_finalize<H>(vacc, zs, eb_run, ml, zsm, a.part_o + pi * D, a.part_ml + pi, lane);

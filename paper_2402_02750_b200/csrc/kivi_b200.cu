@@ -339,6 +339,9 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       fast::WS2::STRIDE));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32, smem));
@@ -362,6 +365,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const bool has_tail = n_sub > nfull;
     static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
     static const int tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
+    static const int tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
     cudaStream_t tail_st = (tail_side && nfull > 0) ? h->side : st;
     if (has_tail) {
         // Tail items (residual fp32 tokens, latency-bound) on a side stream
@@ -373,10 +377,17 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.k_first = (int)nfull;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
-        const int per_sm = (nfull > 0 && tail_st != st) ? tail_ctas : h->fast_per_sm[B][1];
-        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
-                                               ceil_div(a.n_items, fast::WARPS));
-        fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
+        if (nfull > 0 && tail_st != st && tail_warp_ctas) {
+            // one-warp CTAs beside the body kernel: every tail item its own warp
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_warp_ctas,
+                                                   a.n_items);
+            fast::attend_tail_kernel<B, 1><<<(unsigned)grid, 32, fast::WS2::STRIDE, tail_st>>>(a);
+        } else {
+            const int per_sm = (nfull > 0 && tail_st != st) ? tail_ctas : h->fast_per_sm[B][1];
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
+                                                   ceil_div(a.n_items, fast::WARPS));
+            fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
+        }
         KIVI_LAUNCHED();
         if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
         h->total_launches++;
@@ -451,6 +462,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         KIVI_CUDA(cudaFuncSetAttribute(gqa_tc::attend_gqa_tc_kernel<H>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
+        KIVI_CUDA(cudaFuncSetAttribute(gqa::attend_gqa_kernel<H, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, WS::STRIDE));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, gqa::attend_gqa_kernel<H>, gqa::WARPS * 32, smem));
@@ -472,7 +485,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         KIVI_CUDA(dalloc(&h->work, 1));
     }
     const bool has_tail = n_sub > nfull;
-    static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 1);
+    static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
     cudaStream_t tail_st = nfull > 0 ? h->side : st;
     if (has_tail) {
         // items holding fp32 residual rows: CUDA-core kernel, concurrently
@@ -483,10 +496,15 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         a.k_first = (int)nfull;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
-        const int per_sm = tail_st != st ? tail_ctas : h->fast_per_sm[key][2];
-        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
-                                               ceil_div(a.n_items, gqa::WARPS));
-        gqa::attend_gqa_kernel<H><<<(unsigned)grid, gqa::WARPS * 32, smem, tail_st>>>(a);
+        if (tail_st != st) {
+            // one-warp CTAs (27 KB) so two tensor-core CTAs still fit beside one
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_ctas, a.n_items);
+            gqa::attend_gqa_kernel<H, 1><<<(unsigned)grid, 32, WS::STRIDE, tail_st>>>(a);
+        } else {
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][2],
+                                                   ceil_div(a.n_items, gqa::WARPS));
+            gqa::attend_gqa_kernel<H><<<(unsigned)grid, gqa::WARPS * 32, smem, tail_st>>>(a);
+        }
         KIVI_LAUNCHED();
         if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
         h->total_launches++;

@@ -10,18 +10,18 @@ using namespace kivi_b200;
 __global__ void run(const uint8_t* job, const float* q, float* probs_out, int mode) {
     __shared__ __align__(128) uint8_t slot[8192];
     __shared__ __align__(16) float probs[128 * 4];
-    __shared__ __align__(16) uint8_t bf[2304];
+    __shared__ __align__(16) uint8_t bf[4608];
     __shared__ float biasm[32 * 17];
     const int lane = threadIdx.x;
     for (int i = lane; i < 2048; i += 32) reinterpret_cast<uint32_t*>(slot)[i] = reinterpret_cast<const uint32_t*>(job)[i];
     __syncwarp();
-    float qv[4][4]; float qmax = 0.f;
-    for (int h = 0; h < 4; ++h) for (int i = 0; i < 4; ++i) { qv[h][i] = q[h * 128 + 4 * lane + i]; qmax = fmaxf(qmax, fabsf(qv[h][i])); }
+    float2 qv[4][2]; float qmax = 0.f;
+    for (int h = 0; h < 4; ++h) for (int i = 0; i < 2; ++i) { qv[h][i] = make_float2(q[h * 128 + 4 * lane + 2 * i], q[h * 128 + 4 * lane + 2 * i + 1]); qmax = fmaxf(qmax, fmaxf(fabsf(qv[h][i].x), fabsf(qv[h][i].y))); }
     qmax = warp_max(qmax);
     const uint32_t sel = (uint32_t)(lane >> 2 & 3) * 0x1111u + 0x4400u;
-    gqa_tc::key_job<4>(slot, qv, qmax, probs, bf, biasm, lane, sel);
+    gqa_tc::key_job<4>(slot, qv, qmax, probs, 0, bf, biasm, lane, sel);
     __syncwarp();
-    for (int i = lane; i < 512; i += 32) probs_out[i] = probs[i];
+    for (int i = lane; i < 512; i += 32) probs_out[i] = probs[gqa_tc::pidx<4>(i >> 2, i & 3)];
 }
 int main(int argc, char** argv) {
     std::mt19937 rng(1);
