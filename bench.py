@@ -56,6 +56,16 @@ def attend_bytes_per_unit(l, bits, qpk=1, d=D, g=G, r=R):
             + (kr + vr) * d * 4 + qpk * d * 8)
 
 
+def state_bytes_per_unit(capacity, bits, layers, d=D, g=G, r=R):
+    """Device bytes of one (batch, kv-head) unit over all layers: code streams,
+    (lo, hi) pairs and the two fp32 residual rings."""
+    cap = -(-capacity // r) * r
+    codes = 2 * cap * d * bits // 8
+    pairs = 2 * (cap // g) * d * 8
+    rings = 2 * r * d * 4
+    return layers * (codes + pairs + rings + 4 * 256)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -145,11 +155,12 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_reference_sample(cfg_name, steps, warmup, threads, units=None):
+def cpu_reference_sample(cfg_name, steps, warmup, threads, units=None, bits=0):
     """Times the REFERENCE decode_attention (oracle/_ref, compiled from the
     reference sources) on a bounded sample of the workload's units; returns
     (unit-steps per second, description, kind)."""
-    layers, heads, batch, ctx, bits, qpk, _ = CONFIGS[cfg_name]
+    layers, heads, batch, ctx, cbits, qpk, _ = CONFIGS[cfg_name]
+    bits = bits or cbits
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracles import Ref
     if not Ref.available():
@@ -169,10 +180,13 @@ def run_reference_arm(args):
     if rank != 0:
         return
     layers, heads, batch, ctx, bits, qpk, desc = CONFIGS[args.config]
+    if args.bits:
+        bits = args.bits
+        desc = desc.replace("2-bit", f"{bits}-bit")
     threads = os.cpu_count() or 1
     # each "step" is a bounded sample: ~16 units per thread, one decode each
     rate, sample, kind = cpu_reference_sample(args.config, args.steps, args.warmup, threads,
-                                              units=16 * threads)
+                                              units=16 * threads, bits=bits)
     unit_steps_per_step = layers * heads * batch * qpk
     step_s = unit_steps_per_step / rate
     tok_s = batch / step_s
@@ -207,8 +221,12 @@ def run_ours(args):
     layers, heads, batch, ctx, bits, qpk, desc = CONFIGS[args.config]
     if args.layers:
         layers = args.layers
+    if args.bits:
+        bits = args.bits
+        desc = desc.replace("2-bit", f"{bits}-bit")
     from paper_2402_02750_b200.sharding import partition_units
-    scaling = args.scaling or ("strong" if args.config == "c5" else "weak")
+    scaling = args.scaling or ("strong" if args.config in ("c4", "c5") else "weak")
+    capacity_note = None
     if scaling == "strong":
         # fixed global batch, units partitioned over ranks (no collective)
         U = len(partition_units(batch, heads, world, rank))
@@ -218,6 +236,21 @@ def run_ours(args):
         U = batch * heads
         global_batch = batch * world
     steps, warmup = args.steps, args.warmup
+    # C4 (Llama-2-13B, batch 256: 2-bit ~287 GB, 4-bit ~344 GB of state) does
+    # not fit one 180 GB B200 (SURVEY §7 hard part 5).  When a rank's share
+    # does not fit, it runs the largest power-of-two batch that does, and the
+    # line says so; at 8 GPUs (32 sequences per GPU) the full job fits.
+    free, _ = torch.cuda.mem_get_info(dev)
+    per_unit = state_bytes_per_unit(ctx + steps + warmup + R, bits, layers) + 2 * 4 * D * ctx
+    if U * per_unit > 0.85 * free:
+        b_rank = max(1, U // heads)
+        while b_rank > 1 and b_rank * heads * per_unit > 0.85 * free:
+            b_rank //= 2
+        capacity_note = (f"{U // heads} sequences/GPU need {U * per_unit / 1e9:.0f} GB of "
+                         f"state > {free / 1e9:.0f} GB free: timed {b_rank} sequences/GPU")
+        U = b_rank * heads
+        global_batch = b_rank * world
+        scaling = "weak"
     l0 = ctx - warmup - steps
     if l0 < 1:
         raise SystemExit("--steps + --warmup must be < ctx")
@@ -230,7 +263,7 @@ def run_ours(args):
     kbuf = torch.empty((U, l0, D), device=dev, dtype=torch.float32)
     vbuf = torch.empty_like(kbuf)
     for _ in range(layers):
-        c = kb.KVCache(cfg, U, capacity_tokens=ctx + steps + R, device=local)
+        c = kb.KVCache(cfg, U, capacity_tokens=ctx + steps + warmup + R, device=local)
         kbuf.uniform_(-1.0, 1.0, generator=gen)
         vbuf.uniform_(-1.0, 1.0, generator=gen)
         c.prefill(kbuf, vbuf)
@@ -314,17 +347,31 @@ def run_ours(args):
         hq.copy_(qs.cpu())
         hk.copy_(ks.cpu())
         hv.copy_(vs.cpu())
-        # same workload, continuing the decode: l runs ctx+1 .. ctx+steps
+        # same workload, continuing the decode: l runs past ctx.  W untimed
+        # steps first, as for the device-resident loop: a cache's first host
+        # call creates its staging buffers, copy stream and events (one-time,
+        # ~40 ms per cache).
         e2e_steps = steps
+        for i in range(warmup):
+            for ly in range(layers):
+                caches[ly].decode_host(hq[i % pool, ly], hk[i % pool, ly], hv[i % pool, ly],
+                                       ho[ly], q_per_kv=qpk)
         barrier()
         t0 = time.perf_counter()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
+        dbg = os.environ.get("KIVI_E2E_DEBUG")
         for i in range(e2e_steps):
             p = i % pool
+            tw = time.perf_counter()
             for ly in range(layers):
                 caches[ly].decode_host(hq[p, ly], hk[p, ly], hv[p, ly], ho[ly], q_per_kv=qpk)
+            if dbg:
+                te = time.perf_counter() - tw
+                torch.cuda.synchronize()
+                print(f"e2e step {i}: enqueue {te * 1e3:.2f} ms, wall {(time.perf_counter() - tw) * 1e3:.2f} ms",
+                      file=sys.stderr, flush=True)
         f1.record(stream)
         barrier()
         wall = time.perf_counter() - t0
@@ -341,7 +388,7 @@ def run_ours(args):
             threads = os.cpu_count() or 1
             rate, sample, kind = cpu_reference_sample(args.config, steps=min(8, steps),
                                                       warmup=1, threads=threads,
-                                                      units=32 * threads)
+                                                      units=32 * threads, bits=bits)
             step_s = layers * heads * batch * qpk / rate
             cpu = {"value": batch / step_s, "unit": "tokens/s", "cores": threads, "kind": kind,
                    "sample": sample}
@@ -371,6 +418,7 @@ def run_ours(args):
                        "global_batch": global_batch,
                        "ctx": ctx, "bits": bits, "group_size": G, "residual": R, "head_dim": D,
                        "q_per_kv": qpk, "units_per_layer_per_gpu": U,
+                       "capacity_limited": capacity_note,
                        "l_timed": [l_start + 1, l_start + steps],
                        "l2": "state >> 126 MB L2 (inputs larger than L2, no flush)",
                        "parallelism": f"dp{world} ({scaling}; units sharded by "
@@ -403,10 +451,12 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
+    ap.add_argument("--bits", type=int, default=0, choices=[0, 2, 4],
+                    help="override the config's bit width (C4 sweeps 2 and 4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
-                    help="weak: batch per GPU (default); strong: fixed global batch (c5 default)")
+                    help="weak: batch per GPU (default); strong: fixed global batch (c4, c5)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -267,7 +267,7 @@ uint64_t grouped_bytes(int64_t tokens, const kivi_config& cfg) {
 template <typename T>
 kivi_status ensure(T** p, int64_t* cap, int64_t need) {
     if (need <= *cap) return KIVI_OK;
-    cudaFree(*p);
+    if (*p) cudaFree(*p);
     *p = nullptr;
     *cap = 0;
     KIVI_CUDA(dalloc(p, (size_t)need));
@@ -314,9 +314,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
     // body = whole 256-token sub-chunks below floor32(vg) (all quantized)
     const int64_t nfull = ((h->vg() / 32) * 32) / fast::SUB;
-    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * fast::D);
+    // partials sized for the reserved capacity: growing them mid-decode would
+    // cudaFree (a device-wide sync) inside a serving loop
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB));
+    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
     if (rc) return rc;
-    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub);
+    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap);
     if (rc) return rc;
     rc = ensure(&h->stats, &h->stats_cap, U);
     if (rc) return rc;
@@ -437,9 +440,10 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     // tensor-core body = whole 256-token sub-chunks below floor32(vg)
     static const int use_tc = env_int("KIVI_GQA_TC", 1);
     const int64_t nfull = use_tc ? ((h->vg() / 32) * 32) / fast::SUB : 0;
-    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub * H * fast::D);
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB));
+    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * H * fast::D);
     if (rc) return rc;
-    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub * H);
+    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap * H);
     if (rc) return rc;
     rc = ensure(&h->stats, &h->stats_cap, U * H);
     if (rc) return rc;
@@ -543,7 +547,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
 kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, float* weights,
                            int scale_logits, cudaStream_t st) {
     const int64_t rows = h->n_units * qpk;
-    kivi_status rc = ensure(&h->scratch, &h->scratch_cap, rows * h->l);
+    kivi_status rc = ensure(&h->scratch, &h->scratch_cap, rows * std::max(h->l, h->cap));
     if (rc) return rc;
     AttendGenericArgs a;
     a.c = h->dev;
