@@ -33,7 +33,14 @@ namespace fast {
 
 constexpr int D = 128;
 constexpr int G = 32;
-constexpr int SUB = 256;       // tokens per item
+constexpr int SUB = 256;       // tokens per item (tail / GQA items; max tail item)
+// Tokens per MHA body item.  512 measured: body 3.5 % faster per token, but
+// the residual-window region (tail items) grows by 256 tokens per unit and
+// the launch got slower (C2 266 vs 247 us), so 256.
+#ifndef KIVI_MHA_BSUB
+#define KIVI_MHA_BSUB 256
+#endif
+constexpr int BSUB = KIVI_MHA_BSUB;
 constexpr int WARPS = 4;       // warps per CTA
 constexpr int SLOT = 8192;     // bytes per pipeline slot
 constexpr int F_ROWS = 16;     // fp32 residual rows per job (16 * 512 B)
@@ -110,8 +117,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
 struct FastArgs {
     CacheDev c;
     int l, kg, vg;
-    int n_sub;          // partial slots per unit (= ceil(l / SUB))
-    int k_first;        // first sub-chunk index handled by this launch
+    int n_sub;          // partial slots per unit
+    int k_first;        // first partial slot (sub-chunk index) of this launch
+    int t_first;        // first token of this launch's items
+    int sub;            // tokens per item of this launch (plan_item)
     int n_per_unit;     // sub-chunks per unit handled by this launch
     int n_items;        // n_units * n_per_unit
     const float* q;     // [units][128]
@@ -130,12 +139,27 @@ struct WarpSmem {
     static_assert(NSLOT == 2, "q staging assumes two slots");
     static constexpr int QRAW_OFF = NSLOT * SLOT;            // 128 fp32 (staged q)
     static constexpr int QQ_OFF = QRAW_OFF + D * 4;          // 128 fp32 (q * scale * log2e)
-    static constexpr int PROBS_OFF = QQ_OFF + D * 4;         // 256 fp32
+    static constexpr int PROBS_OFF = QQ_OFF + D * 4;         // SUB fp32
     static constexpr int BAR_OFF = PROBS_OFF + SUB * 4;
     static constexpr int BYTES = BAR_OFF + 8 * NSLOT;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
 };
 using WS2 = WarpSmem<2>;
+
+// Body kernel layout: BSUB probabilities, and the staged q row aliased onto
+// the first 128 of them.  Safe because the next item's first job (which
+// carries q) is issued when the second-to-last value job is released; by
+// then only the last value job still reads p, and it reads tokens
+// >= BSUB - VQ_TOK >= 128 (NVJ >= 2).  Keeps 3 CTAs x 4 warps per SM.
+struct WarpSmemBody {
+    static constexpr int QQ_OFF = 2 * SLOT;
+    static constexpr int PROBS_OFF = QQ_OFF + D * 4;
+    static constexpr int QRAW_OFF = PROBS_OFF;
+    static constexpr int BAR_OFF = PROBS_OFF + BSUB * 4;
+    static constexpr int BYTES = BAR_OFF + 16;
+    static constexpr int STRIDE = (BYTES + 127) & ~127;
+};
+using WSB = WarpSmemBody;
 
 // ===================== shared compute bodies ===============================
 
@@ -441,16 +465,17 @@ __device__ __forceinline__ void v_finalize(uint8_t* slot, const float2* vacc, fl
 template <int B>
 __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) {
     using PB = P<B>;
-    constexpr int NKJ = (SUB / 32) / PB::KQ_TILES;  // key jobs per item
-    constexpr int NVJ = SUB / PB::VQ_TOK;           // value jobs per item
+    constexpr int NKJ = (BSUB / 32) / PB::KQ_TILES;  // key jobs per item
+    constexpr int NVJ = BSUB / PB::VQ_TOK;           // value jobs per item
+    static_assert(NVJ >= 2 && BSUB - PB::VQ_TOK >= D, "q staging aliases p[0..127]");
     constexpr int NJ = NKJ + NVJ;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* wbase = smem_raw + warp * WS2::STRIDE;
-    float* qraw = reinterpret_cast<float*>(wbase + WS2::QRAW_OFF);
-    float* qq = reinterpret_cast<float*>(wbase + WS2::QQ_OFF);
-    float* probs = reinterpret_cast<float*>(wbase + WS2::PROBS_OFF);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WS2::BAR_OFF);
+    uint8_t* wbase = smem_raw + warp * WSB::STRIDE;
+    float* qraw = reinterpret_cast<float*>(wbase + WSB::QRAW_OFF);
+    float* qq = reinterpret_cast<float*>(wbase + WSB::QQ_OFF);
+    float* probs = reinterpret_cast<float*>(wbase + WSB::PROBS_OFF);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + WSB::BAR_OFF);
     if (lane == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -483,7 +508,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             uint64_t* bar = &bars[s];
             fence_proxy_async_smem();
             if (f_job < NKJ) {
-                const int64_t tile0 = (int64_t)f_k * (SUB / 32) + f_job * PB::KQ_TILES;
+                const int64_t tile0 = (int64_t)f_k * (BSUB / 32) + f_job * PB::KQ_TILES;
                 constexpr uint32_t cb = PB::KQ_TILES * PB::TILE_CODE;
                 constexpr uint32_t pb = PB::KQ_TILES * D * 8;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? D * 4 : 0));
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
                                      policy);
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * D, D * 4, bar);
             } else {
-                const int64_t ts = (int64_t)f_k * SUB + (f_job - NKJ) * PB::VQ_TOK;
+                const int64_t ts = (int64_t)f_k * BSUB + (f_job - NKJ) * PB::VQ_TOK;
                 constexpr uint32_t cb = PB::VQ_TOK * PB::TOK_CODE;
                 constexpr uint32_t pb = PB::VQ_TOK * (D / G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
@@ -540,7 +565,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             release_slot();
         }
         const float2 ml = softmax_item(
-            probs, SUB, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * SUB : nullptr, lane);
+            probs, BSUB, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * BSUB : nullptr, lane);
         float2 vacc[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) vacc[i] = make_float2(0.f, 0.f);
@@ -574,8 +599,8 @@ __device__ __forceinline__ ItemPlan plan_item(const FastArgs& a, int item) {
     ItemPlan p;
     p.u = item / a.n_per_unit;
     p.k = a.k_first + (item - p.u * a.n_per_unit);
-    p.t0 = p.k * SUB;
-    p.t1 = min(p.t0 + SUB, a.l);
+    p.t0 = a.t_first + (p.k - a.k_first) * a.sub;
+    p.t1 = min(p.t0 + a.sub, a.l);
     const int kq = max(0, min(p.t1, a.kg) - p.t0);
     const int kf = p.t1 - max(p.t0, a.kg);
     const int vq = max(0, min(p.t1, a.vg) - p.t0);

@@ -1,14 +1,17 @@
-// Grouped-query fused dequant-attention decode on the tensor cores
-// (mma.sync m16n8k16, fp16 operands, fp32 accumulation).  H = 2 or 4 query
-// heads share one kv unit (BASELINE config 3: Mistral-7B, H = 4); B = 2,
-// d = 128, G = 32.  Body items only (whole 256-token sub-chunks whose keys
+// Fused dequant-attention decode on the tensor cores (mma.sync m16n8k16,
+// fp16 operands, fp32 accumulation).  H = 1, 2 or 4 query heads share one kv
+// unit (H = 1: MHA, BASELINE configs 1/2/5; H = 4: config 3, Mistral-7B);
+// B = 2, d = 128, G = 32.  Body items only (whole 256-token sub-chunks whose keys
 // and values are all quantized); items holding fp32 residual rows run on the
 // CUDA-core kernel (kernels_attend_gqa.cuh) concurrently.
 //
-// Why tensor cores here and not for MHA: with H heads every code feeds H
-// multiply-adds.  On CUDA cores that is 1 LOP3 + H/2 FFMA2 per code (3 issue
-// slots at H = 4); the MMA does the H-way (and the 16-deep) reduction in one
-// instruction per 256 codes, leaving ~1 ALU op per code for the extraction.
+// Why tensor cores for a GEMV: with H heads every code feeds H multiply-adds.
+// On CUDA cores that is 1 LOP3 + H/2 FFMA2 per code (3 issue slots at H = 4,
+// and the ALU pipe saturates on the extraction at H = 1); the MMA does the
+// H-way and the 16-deep reduction in one instruction per 256 codes, leaving
+// ~0.6 ALU ops per code for the extraction.  N = 8 columns hold (head, hi/lo)
+// pairs, so at H = 1 three quarters of each MMA are zero padding; the tensor
+// pipe is otherwise idle, so that costs nothing measurable.
 //
 // Exactness.  Codes enter the MMA as fp16 SUBNORMALS: a 2-bit code at
 // mantissa bit p of a half is code * 2^(p-24) exactly (a LOP3 isolates it; no
@@ -283,12 +286,16 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
     float2 v[4][H];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float4* src = reinterpret_cast<const float4*>(probs + (lane + 32 * i) * 2 * H);
+        if constexpr (H == 1) {
+            v[i][0] = reinterpret_cast<const float2*>(probs)[lane + 32 * i];
+        } else {
+            const float4* src = reinterpret_cast<const float4*>(probs + (lane + 32 * i) * 2 * H);
 #pragma unroll
-        for (int h2 = 0; h2 < H / 2; ++h2) {
-            const float4 x = src[h2];
-            v[i][2 * h2] = make_float2(x.x, x.y);
-            v[i][2 * h2 + 1] = make_float2(x.z, x.w);
+            for (int h2 = 0; h2 < H / 2; ++h2) {
+                const float4 x = src[h2];
+                v[i][2 * h2] = make_float2(x.x, x.y);
+                v[i][2 * h2 + 1] = make_float2(x.z, x.w);
+            }
         }
     }
     float m[H], sm[H];
@@ -320,11 +327,15 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
             v[i][h].y = fast::ex2_approx(v[i][h].y - m[h]);
             sm[h] += v[i][h].x + v[i][h].y;
         }
-        float4* dst = reinterpret_cast<float4*>(probs + (lane + 32 * i) * 2 * H);
+        if constexpr (H == 1) {
+            reinterpret_cast<float2*>(probs)[lane + 32 * i] = v[i][0];
+        } else {
+            float4* dst = reinterpret_cast<float4*>(probs + (lane + 32 * i) * 2 * H);
 #pragma unroll
-        for (int h2 = 0; h2 < H / 2; ++h2)
-            dst[h2] = make_float4(v[i][2 * h2].x, v[i][2 * h2].y, v[i][2 * h2 + 1].x,
-                                  v[i][2 * h2 + 1].y);
+            for (int h2 = 0; h2 < H / 2; ++h2)
+                dst[h2] = make_float4(v[i][2 * h2].x, v[i][2 * h2].y, v[i][2 * h2 + 1].x,
+                                      v[i][2 * h2 + 1].y);
+        }
     }
 #pragma unroll
     for (int h = 0; h < H; ++h) ml[h] = make_float2(m[h], warp_sum(sm[h]));
@@ -375,20 +386,25 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
         const float2 pa = pairs2[ta * 4 + cgp], pb = pairs2[tb * 4 + cgp];
         const float2 d2 = __fmul2_rn(make_float2(pa.y - pa.x, pb.y - pb.x), make_float2(f, f));
         const float2 z2 = make_float2(pa.x, pb.x);
-        const float4* pp = reinterpret_cast<const float4*>(p_src + pidx<H>(ta, 0));
+        float2 P[H];  // (p_h[ta], p_h[tb])
+        if constexpr (H == 1) {
+            P[0] = *reinterpret_cast<const float2*>(p_src + pidx<H>(ta, 0));
+        } else {
+            const float4* pp = reinterpret_cast<const float4*>(p_src + pidx<H>(ta, 0));
 #pragma unroll
-        for (int h2 = 0; h2 < H / 2; ++h2) {
-            const float4 x = pp[h2];  // (p_2h2[ta], p_2h2[tb], p_2h2+1[ta], p_2h2+1[tb])
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int h = 2 * h2 + e;
-                const float2 P = e ? make_float2(x.z, x.w) : make_float2(x.x, x.y);
-                uint32_t whi, wlo;
-                split_pair(__fmul2_rn(P, d2), whi, wlo);
-                zs[h] = __ffma2_rn(P, z2, zs[h]);
-                bv[cgp * BFV_CG + 2 * ((2 * h) * 4 + tcons) + which] = whi;
-                bv[cgp * BFV_CG + 2 * ((2 * h + 1) * 4 + tcons) + which] = wlo;
+            for (int h2 = 0; h2 < H / 2; ++h2) {
+                const float4 x = pp[h2];
+                P[2 * h2] = make_float2(x.x, x.y);
+                P[2 * h2 + 1] = make_float2(x.z, x.w);
             }
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            uint32_t whi, wlo;
+            split_pair(__fmul2_rn(P[h], d2), whi, wlo);
+            zs[h] = __ffma2_rn(P[h], z2, zs[h]);
+            bv[cgp * BFV_CG + 2 * ((2 * h) * 4 + tcons) + which] = whi;
+            bv[cgp * BFV_CG + 2 * ((2 * h + 1) * 4 + tcons) + which] = wlo;
         }
     };
     // consumer: 4 channel groups x 2 MMAs of K step s

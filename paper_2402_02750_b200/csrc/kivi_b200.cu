@@ -309,14 +309,18 @@ template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st) {
     const int64_t U = h->n_units;
-    if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
+    // Items: body = whole BSUB-token sub-chunks below floor32(vg) (all keys and
+    // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
+    // hold the fp32 residual rows.  One partial slot per item.
+    static const int tsub = std::max(32, std::min(fast::SUB, env_int("KIVI_TAIL_SUB", 256)) / 32 * 32);
+    const int64_t nfull = ((h->vg() / 32) * 32) / fast::BSUB;
+    const int64_t t_first = nfull * fast::BSUB;
+    const int64_t n_sub = nfull + ceil_div(h->l - t_first, tsub);
+    if (h->l >= (1LL << 30) || U * n_sub >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
-    const int64_t n_sub = ceil_div(h->l, fast::SUB);
-    // body = whole 256-token sub-chunks below floor32(vg) (all quantized)
-    const int64_t nfull = ((h->vg() / 32) * 32) / fast::SUB;
     // partials sized for the reserved capacity: growing them mid-decode would
     // cudaFree (a device-wide sync) inside a serving loop
-    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB));
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, tsub) + 2);
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap);
@@ -337,9 +341,18 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     a.wlog = weights;
 
     const int smem = fast::WS2::STRIDE * fast::WARPS;
+    const int smem_body = fast::WSB::STRIDE * fast::WARPS;
+    const int smem_tc = gqa_tc::TS<1>::STRIDE * gqa_tc::WARPS;
+    static const int mha_tc = env_int("KIVI_MHA_TC", 0);  // measured slower on C2
     if (h->fast_per_sm[B][0] == 0) {
+        KIVI_CUDA(cudaFuncSetAttribute(gqa_tc::attend_gqa_tc_kernel<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
+        int tc_per_sm = 0;
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &tc_per_sm, gqa_tc::attend_gqa_tc_kernel<1>, gqa_tc::WARPS * 32, smem_tc));
+        h->fast_per_sm[B][2] = tc_per_sm < 1 ? 1 : tc_per_sm;
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<B>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_body));
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, 1>,
@@ -347,7 +360,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                                        fast::WS2::STRIDE));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32, smem));
+            &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32, smem_body));
         h->fast_per_sm[B][0] = per_sm < 1 ? 1 : per_sm;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
@@ -378,6 +391,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
         }
         a.k_first = (int)nfull;
+        a.t_first = (int)t_first;
+        a.sub = tsub;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
         if (nfull > 0 && tail_st != st && tail_warp_ctas) {
@@ -397,13 +412,23 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     }
     if (nfull > 0) {
         a.k_first = 0;
+        a.t_first = 0;
+        a.sub = fast::BSUB;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
         a.work = h->work;
         KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int), st));
-        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
-                                               ceil_div(a.n_items, fast::WARPS));
-        fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, st>>>(a);
+        if (B == 2 && mha_tc && fast::BSUB == fast::SUB) {
+            // tensor-core body (kernels_attend_gqa_tc.cuh with one query head)
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][2],
+                                                   ceil_div(a.n_items, gqa_tc::WARPS));
+            gqa_tc::attend_gqa_tc_kernel<1>
+                <<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
+        } else {
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
+                                                   ceil_div(a.n_items, fast::WARPS));
+            fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
+        }
         KIVI_LAUNCHED();
         h->total_launches++;
     }
@@ -498,6 +523,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
             KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
         }
         a.k_first = (int)nfull;
+        a.t_first = (int)(nfull * fast::SUB);
+        a.sub = fast::SUB;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
         if (tail_st != st) {
@@ -515,6 +542,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     }
     if (nfull > 0) {
         a.k_first = 0;
+        a.t_first = 0;
+        a.sub = fast::SUB;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
         a.work = h->work;
