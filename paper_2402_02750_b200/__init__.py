@@ -198,6 +198,10 @@ class KVCache:
                                        int(capacity_tokens), ctypes.byref(h)))
         self._h = h
 
+    @property
+    def _decode_fn(self):
+        return lib().kivi_decode
+
     @classmethod
     def _wrap(cls, cfg, n_units, device, handle):
         obj = cls.__new__(cls)
@@ -270,10 +274,26 @@ class KVCache:
 
     def decode(self, q, t_k, t_v, q_per_kv: int = 1, weights: bool = False,
                scale_logits: bool = True, out=None):
-        """Reference decode_attention: append, then attend (attention.cpp:26-100)."""
-        self.append(t_k, t_v)
-        return self.attend(q, q_per_kv=q_per_kv, weights=weights, scale_logits=scale_logits,
-                           out=out)
+        """Reference decode_attention: append, then attend (attention.cpp:26-100).
+        One C-ABI call (kivi_decode); the serving loop calls this per layer, so
+        the host path is kept to a few checks."""
+        if weights:
+            self.append(t_k, t_v)
+            return self.attend(q, q_per_kv=q_per_kv, weights=True, scale_logits=scale_logits,
+                               out=out)
+        torch = _torch()
+        d, U = self.cfg.head_dim, self.n_units
+        if t_k.numel() != U * d or t_v.numel() != U * d or t_k.dtype != torch.float32 \
+                or t_v.dtype != torch.float32:
+            raise ShapeError(f"append_token: expected 1x{d} rows per unit")
+        if q.numel() != U * q_per_kv * d or q.dtype != torch.float32:
+            raise ShapeError(f"query must be [n_units, q_per_kv, {d}] fp32")
+        if out is None:
+            out = torch.empty((U, q_per_kv, d), device=q.device, dtype=torch.float32)
+        _check(self._decode_fn(self._h, _dptr(q), _dptr(t_k), _dptr(t_v), int(q_per_kv),
+                               _dptr(out), None, int(bool(scale_logits)),
+                               torch.cuda.current_stream().cuda_stream))
+        return out
 
     # ---- host-buffer path -------------------------------------------------
     def prefill_host(self, keys, values) -> None:

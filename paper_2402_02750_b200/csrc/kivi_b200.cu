@@ -312,15 +312,22 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // Items: body = whole BSUB-token sub-chunks below floor32(vg) (all keys and
     // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
     // hold the fp32 residual rows.  One partial slot per item.
-    static const int tsub = std::max(32, std::min(fast::SUB, env_int("KIVI_TAIL_SUB", 256)) / 32 * 32);
-    const int64_t nfull = ((h->vg() / 32) * 32) / fast::BSUB;
+    static const int tsub_env = std::max(32, std::min(fast::SUB, env_int("KIVI_TAIL_SUB", 256)) / 32 * 32);
+    static const int tsub_small = std::max(32, std::min(fast::SUB, env_int("KIVI_SMALL_SUB", 64)) / 32 * 32);
+    // Few units (e.g. one sequence's 32 heads): 256-token body items leave
+    // most warps idle and the per-unit residual item becomes the critical
+    // path, so every token goes through tsub-token items instead.
+    const int small_items = env_int("KIVI_SMALL_ITEMS", 1);  // read per call (tests flip it)
+    const bool latency_bound = small_items && U * ceil_div(h->l, fast::BSUB) < 4 * num_sms();
+    const int64_t nfull = latency_bound ? 0 : ((h->vg() / 32) * 32) / fast::BSUB;
     const int64_t t_first = nfull * fast::BSUB;
+    const int tsub = latency_bound ? tsub_small : tsub_env;
     const int64_t n_sub = nfull + ceil_div(h->l - t_first, tsub);
     if (h->l >= (1LL << 30) || U * n_sub >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
     // partials sized for the reserved capacity: growing them mid-decode would
     // cudaFree (a device-wide sync) inside a serving loop
-    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, tsub) + 2);
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, std::min(tsub_env, tsub_small)) + 2);
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap);

@@ -213,17 +213,22 @@ def test_decode_generic_vs_reference(cuda, cfg, l0):
     assert e_w <= 1e-6, e_w
 
 
+@pytest.mark.parametrize("small_items", ["0", "1"])
 @pytest.mark.parametrize("bits", [2, 4])
 @pytest.mark.parametrize("l0", [1, 31, 127, 128, 129, 255, 256, 257, 383, 600, 1153])
-def test_decode_fast_vs_reference(cuda, bits, l0):
+def test_decode_fast_vs_reference(cuda, bits, l0, small_items, monkeypatch):
+    # small_items=1: every token through 64-token items (few-unit route)
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", small_items)
     cfg = (bits, 32, 128, 128)
     e_out, e_w = run_decode(cfg, U=3, l0=l0, steps=4, path="fast", seed=l0 + bits)
     assert e_out <= 1e-5, e_out
     assert e_w <= 1e-5, e_w
 
 
+@pytest.mark.parametrize("small_items", ["0", "1"])
 @pytest.mark.parametrize("bits", [2, 4])
-def test_decode_fast_across_flush_and_long_context(cuda, bits):
+def test_decode_fast_across_flush_and_long_context(cuda, bits, small_items, monkeypatch):
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", small_items)
     cfg = (bits, 32, 128, 128)
     # 130 steps cross a key flush and 130 value pops; ctx ~4k like config 1.
     e_out, _ = run_decode(cfg, U=2, l0=3968, steps=130, path="fast", seed=7, weights=False)
