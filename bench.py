@@ -382,6 +382,30 @@ def run_ours(args):
                "steps": e2e_steps, "wall_s": wall,
                "path": "kivi_decode_host (C-ABI, pinned host buffers, copies in the timed region)"}
 
+    # ---- optional NCCL all-gather of every layer's outputs ------
+    gather = None
+    if args.gather:
+        from paper_2402_02750_b200.sharding import gather_outputs
+        counts = [U] * world if scaling == "weak" else \
+            [len(partition_units(batch, heads, world, r)) for r in range(world)]
+        for ly in range(layers):
+            gather_outputs(outs[ly], counts)
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(steps):
+            for ly in range(layers):
+                gather_outputs(outs[ly], counts)
+        g1.record(stream)
+        barrier()
+        g_s = max_over_ranks(g0.elapsed_time(g1) / 1e3)
+        gbytes = layers * sum(counts) * qpk * D * 4
+        gather = {"ms_per_step": g_s / steps * 1e3, "bytes_per_step": gbytes,
+                  "GBps": gbytes * steps / g_s / 1e9 if g_s > 0 else None,
+                  "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 rank)",
+                  "note": "timed separately; not part of value"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -433,6 +457,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "gather": gather,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -454,6 +479,8 @@ def main():
     ap.add_argument("--bits", type=int, default=0, choices=[0, 2, 4],
                     help="override the config's bit width (C4 sweeps 2 and 4)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", action="store_true",
+                    help="also time the optional NCCL all-gather of every layer's outputs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: batch per GPU (default); strong: fixed global batch (c4, c5)")

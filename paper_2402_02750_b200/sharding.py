@@ -39,3 +39,32 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_outputs(out_local, n_local_per_rank):
+    """Optional all-gather of the per-rank decode outputs (the only
+    collective the decode path may have; NCCL over NVLink on GPUs, gloo on CPU).
+
+    out_local: [n_local, ...] tensor of this rank's units (in partition order);
+    n_local_per_rank: unit count of every rank.  Returns [sum(n), ...] in rank
+    order, i.e. the global unit order of `partition_units`.  Uneven shards are
+    padded to the largest one for the collective and trimmed afterwards.
+    """
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return out_local
+    world = dist.get_world_size()
+    m = max(n_local_per_rank)
+    tail = tuple(out_local.shape[1:])
+    pad = out_local.new_zeros((m,) + tail)
+    pad[: out_local.shape[0]] = out_local
+    if dist.get_backend() == "nccl":
+        buf = out_local.new_empty((world * m,) + tail)
+        dist.all_gather_into_tensor(buf, pad)
+        parts = [buf[r * m: r * m + n] for r, n in enumerate(n_local_per_rank)]
+    else:
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad)
+        parts = [b[:n] for b, n in zip(bufs, n_local_per_rank)]
+    return torch.cat(parts)

@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2402_02750_b200.sharding import max_over_ranks, partition_units
+from paper_2402_02750_b200.sharding import gather_outputs, max_over_ranks, partition_units
 
 
 def _free_port():
@@ -34,6 +34,14 @@ def _worker(rank, world, port, shapes, out):
         t = max_over_ranks(1.0 + rank)
         if rank == 0:
             out.put(("max", t))
+        # optional output all-gather: each rank's outputs carry its unit ids
+        batch, heads = 5, 3  # uneven shards (batch-major: 2 and 3 sequences)
+        mine = partition_units(batch, heads, world, rank)
+        counts = [len(partition_units(batch, heads, world, r)) for r in range(world)]
+        local = torch.tensor([[b * heads + h, rank] for b, h in mine], dtype=torch.float32)
+        full = gather_outputs(local, counts)
+        if rank == 0:
+            out.put(("gather", full[:, 0].tolist(), full[:, 1].tolist(), counts))
     finally:
         dist.destroy_process_group()
 
@@ -46,14 +54,17 @@ def test_partition_two_ranks_gloo():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, shapes, q)) for r in range(2)]
     for p in procs:
         p.start()
-    results = [q.get(timeout=120) for _ in range(len(shapes) + 1)]
+    results = [q.get(timeout=120) for _ in range(len(shapes) + 2)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for r in results[:-1]:
+    for r in results[:-2]:
         batch, heads, n, n_unique, covers = r
         assert n == n_unique == batch * heads and covers, r
-    assert results[-1] == ("max", 2.0)
+    assert results[-2] == ("max", 2.0)
+    tag, ids, owners, counts = results[-1]
+    assert tag == "gather" and ids == list(range(15)), ids
+    assert owners == [0.0] * counts[0] + [1.0] * counts[1]
 
 
 @pytest.mark.parametrize("batch,heads,world", [(64, 32, 8), (1, 32, 8), (16, 32, 8), (5, 3, 4)])
