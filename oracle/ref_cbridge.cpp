@@ -7,7 +7,9 @@
 //   prefill / append_token / decode_attention / materialize_* / memory_bytes
 //   (reference proj/include/kivi/kv_cache.hpp:45-58, attention.hpp:18-27),
 //   quantize_group / pack_codes / QuantizedTensor::quantize
-//   (reference proj/include/kivi/quantize.hpp:35-70).
+//   (reference proj/include/kivi/quantize.hpp:35-70),
+//   estimate_memory / max_batch_at_budget / SyntheticLayer /
+//   run_decode_benchmark (reference proj/include/kivi/workload.hpp:41-73).
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -19,9 +21,11 @@
 #include <thread>
 #include <vector>
 
+#include "kivi/analysis.hpp"
 #include "kivi/attention.hpp"
 #include "kivi/kv_cache.hpp"
 #include "kivi/quantize.hpp"
+#include "kivi/workload.hpp"
 
 using namespace kivi;
 
@@ -57,6 +61,32 @@ struct State {
 };
 
 CacheConfig cfg_of(int bits, int64_t G, int64_t R, int64_t d) { return CacheConfig{bits, G, R, d}; }
+
+int code_of_budget(const std::exception& e) {
+    if (dynamic_cast<const BudgetError*>(&e)) return 4;
+    return code_of(e);
+}
+
+#define GUARD_B(...)                         \
+    try {                                    \
+        __VA_ARGS__;                         \
+        return 0;                            \
+    } catch (const std::exception& e) {      \
+        g_err = e.what();                    \
+        return code_of_budget(e);            \
+    }
+
+// spec[6] = batch, prompt_len, gen_len, layers, kv_heads, head_dim
+WorkloadSpec spec_of(const int64_t* s) {
+    WorkloadSpec w;
+    w.batch = s[0];
+    w.prompt_len = s[1];
+    w.gen_len = s[2];
+    w.layers = s[3];
+    w.kv_heads = s[4];
+    w.head_dim = s[5];
+    return w;
+}
 
 }  // namespace
 
@@ -251,6 +281,73 @@ int ref_bench_decode(int bits, int64_t G, int64_t R, int64_t d, int64_t n_units,
         double cs = 0.0;
         for (double v : sums) cs += v;
         *checksum = cs;
+    })
+}
+
+// ---- workload layer (reference workload.cpp) ---------------------------------
+// out[5] = fp, kivi, code, scale_zero, residual bytes; *ratio = compression.
+int ref_estimate_memory(const int64_t* spec, int bits, int64_t G, int64_t R, uint64_t* out,
+                        double* ratio) {
+    GUARD({
+        const MemoryEstimate e = estimate_memory(spec_of(spec), cfg_of(bits, G, R, spec[5]));
+        out[0] = e.fp_bytes;
+        out[1] = e.kivi_bytes;
+        out[2] = e.code_bytes;
+        out[3] = e.scale_zero_bytes;
+        out[4] = e.residual_bytes;
+        *ratio = e.compression_ratio;
+    })
+}
+
+int ref_max_batch_at_budget(const int64_t* spec, uint64_t budget, int fp_mode, int bits,
+                            int64_t G, int64_t R, int64_t* out) {
+    GUARD_B({
+        *out = max_batch_at_budget(spec_of(spec), budget, fp_mode ? BenchMode::fp : BenchMode::kivi,
+                                   cfg_of(bits, G, R, spec[5]));
+    })
+}
+
+// The exact synthetic data run_decode_benchmark draws (workload.cpp:157-160,
+// 198-201, 222-223): per-layer W_q, W_k, W_v [hidden][hidden] (row-major,
+// layers x 3), prompts [batch][prompt_len][hidden], decode tokens
+// [gen_len][batch][hidden].
+int ref_workload_data(const int64_t* spec, uint64_t seed, float* weights, float* prompts,
+                      float* tokens) {
+    GUARD({
+        const WorkloadSpec w = spec_of(spec);
+        const int64_t hidden = w.hidden();
+        const size_t hh = (size_t)(hidden * hidden);
+        for (int64_t ly = 0; ly < w.layers; ++ly) {
+            SyntheticLayer L(hidden, seed + 1000003ull * (uint64_t)ly);
+            std::memcpy(weights + (3 * ly + 0) * hh, L.w_q.data(), sizeof(float) * hh);
+            std::memcpy(weights + (3 * ly + 1) * hh, L.w_k.data(), sizeof(float) * hh);
+            std::memcpy(weights + (3 * ly + 2) * hh, L.w_v.data(), sizeof(float) * hh);
+        }
+        std::mt19937_64 data_rng(seed ^ 0x9e3779b97f4a7c15ull);
+        const size_t ph = (size_t)(w.prompt_len * hidden);
+        for (int64_t b = 0; b < w.batch; ++b) {
+            const Matrix x = gaussian_matrix(w.prompt_len, hidden, data_rng);
+            std::memcpy(prompts + b * ph, x.data(), sizeof(float) * ph);
+        }
+        for (int64_t step = 0; step < w.gen_len; ++step)
+            for (int64_t b = 0; b < w.batch; ++b) {
+                const Matrix t = gaussian_matrix(1, hidden, data_rng);
+                std::memcpy(tokens + (step * w.batch + b) * hidden, t.data(), sizeof(float) * hidden);
+            }
+    })
+}
+
+// out_d[2] = tokens_per_sec, output_checksum; *peak = peak_cache_bytes.
+int ref_run_decode_benchmark(const int64_t* spec, uint64_t seed, int fp_mode, int bits, int64_t G,
+                             int64_t R, uint64_t budget, double* out_d, uint64_t* peak) {
+    GUARD_B({
+        const BenchReport r = run_decode_benchmark(
+            spec_of(spec), cfg_of(bits, G, R, spec[5]), seed,
+            fp_mode ? BenchMode::fp : BenchMode::kivi,
+            budget ? std::optional<std::uint64_t>(budget) : std::nullopt);
+        out_d[0] = r.tokens_per_sec;
+        out_d[1] = r.output_checksum;
+        *peak = r.peak_cache_bytes;
     })
 }
 

@@ -56,6 +56,10 @@ class CapacityError(KiviError):
     pass
 
 
+class BudgetError(KiviError):
+    """reference BudgetError (errors.hpp:33-35): a memory budget was exceeded."""
+
+
 _ERRORS = {1: ShapeError, 2: UsageError, 3: ConfigError, 4: CudaError, 5: OutOfMemory,
            6: CapacityError}
 

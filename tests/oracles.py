@@ -234,6 +234,11 @@ class Ref(_Base):
                 "ref_reference_attention": (CI, [P, I64, P, P, I64, I64, CI, P]),
                 "ref_bench_decode": (CI, [CI, I64, I64, I64, I64, I64, I64, I64, CI,
                                           ctypes.c_uint64, P, P]),
+                "ref_estimate_memory": (CI, [P, CI, I64, I64, P, P]),
+                "ref_max_batch_at_budget": (CI, [P, ctypes.c_uint64, CI, CI, I64, I64, P]),
+                "ref_workload_data": (CI, [P, ctypes.c_uint64, P, P, P]),
+                "ref_run_decode_benchmark": (CI, [P, ctypes.c_uint64, CI, CI, I64, I64,
+                                                  ctypes.c_uint64, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -280,6 +285,46 @@ class Ref(_Base):
 
     def unit(self, bits, G, R, d):
         return RefUnit(self, bits, G, R, d)
+
+    # ---- workload layer (reference workload.cpp) --------------------------
+    @staticmethod
+    def _spec(spec):
+        return np.array([spec.batch, spec.prompt_len, spec.gen_len, spec.layers, spec.kv_heads,
+                         spec.head_dim], np.int64)
+
+    def estimate_memory(self, spec, bits, G, R):
+        sp = self._spec(spec)
+        out = np.zeros(5, np.uint64)
+        ratio = ctypes.c_double()
+        self._chk(self.lib().ref_estimate_memory(_p(sp), bits, G, R, _p(out), ctypes.byref(ratio)))
+        return dict(zip(["fp_bytes", "kivi_bytes", "code_bytes", "scale_zero_bytes",
+                         "residual_bytes"], (int(x) for x in out)), compression_ratio=ratio.value)
+
+    def max_batch_at_budget(self, spec, budget, fp_mode, bits, G, R):
+        sp = self._spec(spec)
+        out = ctypes.c_int64()
+        self._chk(self.lib().ref_max_batch_at_budget(_p(sp), budget, int(fp_mode), bits, G, R,
+                                                     ctypes.byref(out)))
+        return out.value
+
+    def workload_data(self, spec, seed):
+        """The exact weights / prompts / decode tokens run_decode_benchmark draws."""
+        sp = self._spec(spec)
+        hid = spec.head_dim * spec.kv_heads
+        w = np.zeros((spec.layers, 3, hid, hid), np.float32)
+        pr = np.zeros((spec.batch, spec.prompt_len, hid), np.float32)
+        tk = np.zeros((max(spec.gen_len, 1), spec.batch, hid), np.float32)
+        self._chk(self.lib().ref_workload_data(_p(sp), seed, _p(w), _p(pr), _p(tk)))
+        return w, pr, tk[:spec.gen_len]
+
+    def run_decode_benchmark(self, spec, seed, fp_mode, bits, G, R, budget=0):
+        sp = self._spec(spec)
+        out = np.zeros(2, np.float64)
+        peak = ctypes.c_uint64()
+        self._chk(self.lib().ref_run_decode_benchmark(_p(sp), seed, int(fp_mode), bits, G, R,
+                                                      budget, _p(out), ctypes.byref(peak)))
+        return {"tokens_per_sec": float(out[0]), "output_checksum": float(out[1]),
+                "peak_cache_bytes": int(peak.value)}
 
     def bench_decode(self, bits, G, R, d, n_units, l_prefill, warmup, steps, threads, seed=1):
         secs, cs = ctypes.c_double(), ctypes.c_double()

@@ -10,6 +10,8 @@ Bars (DESIGN.md "parity"):
     rel-L2 <= 1e-5 (the reference's own hybrid bound, test_attention.cpp:79);
   * softmax weights: max |diff| <= 1e-6 (generic), <= 1e-5 (fast).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -423,3 +425,51 @@ def test_import_export_roundtrip(cuda):
     q, tk, tv = rnd(rng, 32), rnd(rng, 32), rnd(rng, 32)
     out = c.decode(dev(q)[None, None], dev(tk)[None], dev(tv)[None]).cpu().numpy().reshape(-1)
     assert rel_l2(out, r.decode(q, tk, tv)) <= 1e-6
+
+
+# ---- workload driver (reference run_decode_benchmark, workload.cpp:145-271) ----
+
+def test_run_decode_benchmark_matches_reference_tiny(cuda):
+    """The reference's own synthetic data (tests/golden/workload_tiny.npz): same
+    checksum of every decode output (tolerance: fp32 GEMM order), identical peak
+    cache bytes counted from live states, both modes."""
+    import json
+    from paper_2402_02750_b200 import workload as wl
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    gold = json.load(open(os.path.join(here, "workload_golden.json")))["tiny_run"]
+    data = np.load(os.path.join(here, "workload_tiny.npz"))
+    sp = wl.WorkloadSpec(*gold["spec"])
+    bits, G, R = gold["cfg"]
+    for mode in ("kivi", "fp"):
+        rep = wl.run_decode_benchmark(sp, kb.CacheConfig(bits, G, R, sp.head_dim), mode=mode,
+                                      data=(data["weights"], data["prompts"], data["tokens"]))
+        want = gold["reference"][mode]
+        assert rep.peak_cache_bytes == want["peak_cache_bytes"], mode
+        assert abs(rep.output_checksum - want["output_checksum"]) <= 1e-5 * rep.output_abs_sum, \
+            (mode, rep.output_checksum, want["output_checksum"], rep.output_abs_sum)
+        assert rep.decode_steps == sp.gen_len and rep.tokens_per_sec > 0
+
+
+def test_run_decode_benchmark_fast_path_vs_reference(cuda):
+    """d = 128, G = 32, R = 128 (the fast kernels), data from the reference."""
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2402_02750_b200 import workload as wl
+    sp = wl.WorkloadSpec(batch=3, prompt_len=700, gen_len=5, layers=2, kv_heads=2, head_dim=128)
+    ref = Ref()
+    data = ref.workload_data(sp, 3)
+    want = ref.run_decode_benchmark(sp, 3, 0, 2, 32, 128)
+    rep = wl.run_decode_benchmark(sp, kb.CacheConfig(2, 32, 128, 128), data=data)
+    assert rep.peak_cache_bytes == want["peak_cache_bytes"]
+    assert abs(rep.output_checksum - want["output_checksum"]) <= 1e-5 * rep.output_abs_sum
+
+
+def test_run_decode_benchmark_budget(cuda):
+    from paper_2402_02750_b200 import workload as wl
+    sp = wl.WorkloadSpec(batch=2, prompt_len=100, gen_len=40, layers=1, kv_heads=2, head_dim=128)
+    cfg = kb.CacheConfig(2, 32, 128, 128)
+    est = wl.estimate_memory(sp, cfg).kivi_bytes
+    rep = wl.run_decode_benchmark(sp, cfg, seed=1, budget_bytes=est)
+    assert rep.peak_cache_bytes == est  # counted == estimated (reference acceptance c5)
+    with pytest.raises(kb.BudgetError):
+        wl.run_decode_benchmark(sp, cfg, seed=1, budget_bytes=est - 1)
