@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "kivi/analysis.hpp"
+#include "kivi/dump_io.hpp"
 #include "kivi/attention.hpp"
 #include "kivi/kv_cache.hpp"
 #include "kivi/quantize.hpp"
@@ -349,6 +350,38 @@ int ref_run_decode_benchmark(const int64_t* spec, uint64_t seed, int fp_mode, in
         out_d[1] = r.output_checksum;
         *peak = r.peak_cache_bytes;
     })
+}
+
+// ---- KVQD dumps (reference dump_io.cpp) ---------------------------------------
+// write: n tensors of rows x cols; read: dims[3] = heads, rows, cols, then data
+// (call with data = NULL to get dims).  Errors: FormatError -> 5 with the byte
+// offset in *offset.
+int ref_write_dump(const char* path, const float* data, int64_t n, int64_t rows, int64_t cols) {
+    GUARD({
+        std::vector<Matrix> t;
+        for (int64_t i = 0; i < n; ++i) t.push_back(from(data + i * rows * cols, rows, cols));
+        write_dump(path, t);
+    })
+}
+
+int ref_read_dump(const char* path, int64_t* dims, float* data, uint64_t* offset) {
+    try {
+        const std::vector<Matrix> t = read_dump(path);
+        dims[0] = (int64_t)t.size();
+        dims[1] = t.empty() ? 0 : t[0].rows();
+        dims[2] = t.empty() ? 0 : t[0].cols();
+        if (data)
+            for (size_t i = 0; i < t.size(); ++i)
+                std::memcpy(data + i * t[i].size(), t[i].data(), sizeof(float) * t[i].size());
+        return 0;
+    } catch (const FormatError& e) {
+        g_err = e.what();
+        *offset = e.byte_offset;
+        return 5;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
 }
 
 }  // extern "C"

@@ -60,6 +60,15 @@ class BudgetError(KiviError):
     """reference BudgetError (errors.hpp:33-35): a memory budget was exceeded."""
 
 
+class FormatError(KiviError):
+    """reference FormatError (errors.hpp:25-30): malformed dump file; carries the
+    byte offset of the failing field."""
+
+    def __init__(self, msg: str, offset: int):
+        super().__init__(f"{msg} (at byte offset {offset})")
+        self.byte_offset = offset
+
+
 _ERRORS = {1: ShapeError, 2: UsageError, 3: ConfigError, 4: CudaError, 5: OutOfMemory,
            6: CapacityError}
 

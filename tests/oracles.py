@@ -239,6 +239,8 @@ class Ref(_Base):
                 "ref_workload_data": (CI, [P, ctypes.c_uint64, P, P, P]),
                 "ref_run_decode_benchmark": (CI, [P, ctypes.c_uint64, CI, CI, I64, I64,
                                                   ctypes.c_uint64, P, P]),
+                "ref_write_dump": (CI, [ctypes.c_char_p, P, I64, I64, I64]),
+                "ref_read_dump": (CI, [ctypes.c_char_p, P, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -325,6 +327,23 @@ class Ref(_Base):
                                                       budget, _p(out), ctypes.byref(peak)))
         return {"tokens_per_sec": float(out[0]), "output_checksum": float(out[1]),
                 "peak_cache_bytes": int(peak.value)}
+
+    # ---- KVQD dumps (reference dump_io.cpp) ---------------------------------
+    def write_dump(self, path, tensors):
+        t = np.ascontiguousarray(np.stack([np.asarray(x, np.float32) for x in tensors]))
+        self._chk(self.lib().ref_write_dump(path.encode(), _p(t), t.shape[0], t.shape[1],
+                                            t.shape[2]))
+
+    def read_dump(self, path):
+        """-> (list of arrays, None) or (None, (code, byte_offset or None))."""
+        dims = np.zeros(3, np.int64)
+        off = ctypes.c_uint64()
+        rc = self.lib().ref_read_dump(path.encode(), _p(dims), None, ctypes.byref(off))
+        if rc:
+            return None, (rc, off.value if rc == 5 else None)
+        data = np.zeros(int(dims.prod()), np.float32)
+        self._chk(self.lib().ref_read_dump(path.encode(), _p(dims), _p(data), ctypes.byref(off)))
+        return list(data.reshape(dims)), None
 
     def bench_decode(self, bits, G, R, d, n_units, l_prefill, warmup, steps, threads, seed=1):
         secs, cs = ctypes.c_double(), ctypes.c_double()

@@ -473,3 +473,26 @@ def test_run_decode_benchmark_budget(cuda):
     assert rep.peak_cache_bytes == est  # counted == estimated (reference acceptance c5)
     with pytest.raises(kb.BudgetError):
         wl.run_decode_benchmark(sp, cfg, seed=1, budget_bytes=est - 1)
+
+
+def test_export_cache_unit_kvqd(cuda, tmp_path):
+    """A device cache unit dumped as KVQD equals the reference's materialisation
+    of the same state (read back by the reference's own read_dump when built)."""
+    from paper_2402_02750_b200.dump_io import export_cache_unit, read_dump
+    ck = checker()
+    rng = np.random.default_rng(21)
+    U, d, l0 = 3, 128, 333
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    cache = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    cache.prefill(dev(K), dev(V))
+    kp, vp = str(tmp_path / "k.kvqd"), str(tmp_path / "v.kvqd")
+    export_cache_unit(cache, 1, kp, vp)
+    r = ck.unit(2, 32, 128, d)
+    r.prefill(K[1], V[1])
+    mk, mv = r.materialize()
+    (gk,), (gv,) = read_dump(kp), read_dump(vp)
+    assert gk.tobytes() == np.asarray(mk, np.float32).tobytes()
+    assert gv.tobytes() == np.asarray(mv, np.float32).tobytes()
+    if Ref.available():
+        back, err = Ref().read_dump(kp)
+        assert err is None and back[0].tobytes() == gk.tobytes()
