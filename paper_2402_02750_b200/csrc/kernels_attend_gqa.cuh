@@ -199,37 +199,46 @@ __device__ __forceinline__ void kq_tiles_heads(uint8_t* slot, const float* qt, f
     }
 }
 
-// fp32 key residual rows -> logits of H heads.
+// fp32 key residual rows -> logits of H heads.  Lane = (row r = lane / 2,
+// e = lane % 2): at H = 4, e picks the head pair and the lane runs the whole
+// 128-channel dot product for both heads with FFMA2 (no cross-lane reduction);
+// at H = 2, e picks a channel half and one shuffle adds the halves.  The
+// row's float4 chunks are visited from a row-rotated start so the 16 rows
+// of a job (512 B apart) hit distinct banks.  (Was: per-head lane-per-channel
+// partials + a 16-way shuffle reduce-scatter, ~4x the instructions.)
 template <int H>
 __device__ __forceinline__ void kf_rows_heads(const uint8_t* slot, const float* qt, float* probs_dst,
                                               int n, int lane) {
-#pragma unroll 1
-    for (int h = 0; h < H; ++h) {
-        float qv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) qv[i] = qt[(4 * lane + i) * QT_STRIDE<H> + h];
-        float part[F_ROWS];
-#pragma unroll
-        for (int r = 0; r < F_ROWS; ++r) {
-            part[r] = 0.f;
-            if (r < n) {
-                const float4 kv = reinterpret_cast<const float4*>(slot + r * D * 4)[lane];
-                part[r] = qv[0] * kv.x + qv[1] * kv.y + qv[2] * kv.z + qv[3] * kv.w;
-            }
+    static_assert(H == 2 || H == 4, "kf_rows_heads: H in {2, 4}");
+    const int r = lane >> 1, e = lane & 1;
+    const float4* row = reinterpret_cast<const float4*>(slot + r * D * 4);
+    constexpr int NCH = H == 4 ? 32 : 16;   // float4 chunks per lane
+    const int hp = H == 4 ? e : 0;          // head pair
+    const int c0 = H == 4 ? 0 : 16 * e;     // first chunk of this lane's half
+    float2 acc = make_float2(0.f, 0.f), acc1 = acc;
+    if (r < n) {
+#pragma unroll 4
+        for (int i = 0; i < NCH; ++i) {
+            const int c4 = c0 + ((i + r) & (NCH - 1));
+            const float4 kv = row[c4];
+            const float* q = qt + (4 * c4) * QT_STRIDE<H> + 2 * hp;
+            acc = __ffma2_rn(*reinterpret_cast<const float2*>(q), make_float2(kv.x, kv.x), acc);
+            acc1 = __ffma2_rn(*reinterpret_cast<const float2*>(q + QT_STRIDE<H>),
+                              make_float2(kv.y, kv.y), acc1);
+            acc = __ffma2_rn(*reinterpret_cast<const float2*>(q + 2 * QT_STRIDE<H>),
+                             make_float2(kv.z, kv.z), acc);
+            acc1 = __ffma2_rn(*reinterpret_cast<const float2*>(q + 3 * QT_STRIDE<H>),
+                              make_float2(kv.w, kv.w), acc1);
         }
-#pragma unroll
-        for (int r = 0; r < F_ROWS; ++r) part[r] += __shfl_xor_sync(0xffffffffu, part[r], 16);
-#pragma unroll
-        for (int half = F_ROWS / 2; half >= 1; half >>= 1) {
-            const bool upper = (lane & half) != 0;
-#pragma unroll
-            for (int i = 0; i < half; ++i) {
-                const float send = upper ? part[i] : part[i + half];
-                const float keep = upper ? part[i + half] : part[i];
-                part[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
-            }
-        }
-        if (lane < n) probs_dst[lane * H + h] = part[0];
+    }
+    acc.x += acc1.x;
+    acc.y += acc1.y;
+    if constexpr (H == 2) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+        if (r < n && e == 0) *reinterpret_cast<float2*>(probs_dst + r * H) = acc;
+    } else {
+        if (r < n) *reinterpret_cast<float2*>(probs_dst + r * H + 2 * hp) = acc;
     }
 }
 
