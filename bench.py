@@ -367,6 +367,8 @@ def run_ours(args):
             tw = time.perf_counter()
             for ly in range(layers):
                 caches[ly].decode_host(hq[p, ly], hk[p, ly], hv[p, ly], ho[ly], q_per_kv=qpk)
+            for c in caches:  # this step's outputs are on the host before the next
+                c.host_join(stream)
             if dbg:
                 te = time.perf_counter() - tw
                 torch.cuda.synchronize()

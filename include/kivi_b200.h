@@ -149,7 +149,11 @@ kivi_status kivi_decode(kivi_cache* cache, const float* t_q, const float* t_k, c
                         int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
                         void* stream);
 
-/* Host-buffer variants: the copies in and out are enqueued with the work. */
+/* Host-buffer variants: the copies in and out are enqueued with the work.
+ * kivi_decode_host copies its result on the cache's own copy stream (so the
+ * next layer's kernels on `stream` do not queue behind it): before reading
+ * `out`/`weights`, call kivi_host_join(cache, stream) and synchronise
+ * `stream` (or synchronise the device). */
 kivi_status kivi_prefill_host(kivi_cache* cache, const float* keys, const float* values,
                               int64_t l, void* stream);
 kivi_status kivi_append_host(kivi_cache* cache, const float* t_k, const float* t_v,
@@ -157,6 +161,8 @@ kivi_status kivi_append_host(kivi_cache* cache, const float* t_k, const float* t
 kivi_status kivi_decode_host(kivi_cache* cache, const float* t_q, const float* t_k,
                              const float* t_v, int32_t q_per_kv, float* out, float* weights,
                              int32_t scale_logits, void* stream);
+/* Orders `stream` after every result copy kivi_decode_host has enqueued. */
+kivi_status kivi_host_join(kivi_cache* cache, void* stream);
 
 /* ---- state exchange in the reference layout (parity / drop-in facade) ---- */
 

@@ -113,6 +113,7 @@ HEADER_SYMBOLS = {
     "kivi_prefill_host": (ctypes.c_int, [P, P, P, I64, P]),
     "kivi_append_host": (ctypes.c_int, [P, P, P, P]),
     "kivi_decode_host": (ctypes.c_int, [P, P, P, P, I32, P, P, I32, P]),
+    "kivi_host_join": (ctypes.c_int, [P, P]),
     "kivi_export_unit": (ctypes.c_int, [P, I64, P, P]),
     "kivi_import_unit": (ctypes.c_int, [P, I64, I64, I64, I64, P, P]),
     "kivi_materialize": (ctypes.c_int, [P, P, P, P]),
@@ -320,12 +321,17 @@ class KVCache:
 
     def decode_host(self, q, t_k, t_v, out, q_per_kv: int = 1, weights=None,
                     scale_logits: bool = True, stream=None) -> None:
-        """All arguments are host buffers (numpy, ideally pinned); copies are
-        enqueued with the kernels on `stream`; synchronise before reading."""
+        """All arguments are host buffers (numpy, ideally pinned); the copies are
+        enqueued with the kernels on `stream`, the result copy on the cache's own
+        copy stream: call host_join(stream) and synchronise before reading."""
         _check(lib().kivi_decode_host(
             self._h, _hptr(q), _hptr(t_k), _hptr(t_v), int(q_per_kv), _hptr(out),
             _hptr(weights) if weights is not None else None, int(bool(scale_logits)),
             _stream_ptr(stream)))
+
+    def host_join(self, stream=None) -> None:
+        """Orders `stream` after every result copy decode_host has enqueued."""
+        _check(lib().kivi_host_join(self._h, _stream_ptr(stream)))
 
     # ---- parity helpers -----------------------------------------------------
     def export_unit(self, unit: int) -> dict:

@@ -132,6 +132,9 @@ struct kivi_cache {
     int* work = nullptr;  // body kernel dynamic item counter
     cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
     cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
+    cudaStream_t d2h = nullptr;         // result copies of the host path
+    cudaEvent_t ev_out_ready = nullptr; // staged result written by the kernels
+    cudaEvent_t ev_out_free = nullptr;  // staged result copied to the host
 
     // profiling
     bool profile = false;
@@ -673,6 +676,9 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     cudaFree(h->work);
+    if (h->d2h) cudaStreamDestroy(h->d2h);
+    if (h->ev_out_ready) cudaEventDestroy(h->ev_out_ready);
+    if (h->ev_out_free) cudaEventDestroy(h->ev_out_free);
     if (h->ev_in_free) cudaEventDestroy(h->ev_in_free);
     if (h->ev_h2d_done) cudaEventDestroy(h->ev_h2d_done);
     for (auto& ev : h->events) {
@@ -918,6 +924,10 @@ static kivi_status stage_rows(kivi_cache* h, int64_t qpk, int64_t wlen) {
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_in_free, cudaEventDisableTiming));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_h2d_done, cudaEventDisableTiming));
         KIVI_CUDA(cudaEventRecord(h->ev_in_free, h->h2d));  // nothing staged yet
+        KIVI_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_out_ready, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_out_free, cudaEventDisableTiming));
+        KIVI_CUDA(cudaEventRecord(h->ev_out_free, h->d2h));  // nothing to copy yet
     }
     if ((rc = ensure(&h->st_q, &h->st_cap_q, U * qpk * d))) return rc;
     if ((rc = ensure(&h->st_out, &h->st_cap_out, U * qpk * d))) return rc;
@@ -966,14 +976,30 @@ kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, 
     KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
     KIVI_CUDA(cudaEventRecord(h->ev_h2d_done, h->h2d));
     KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_h2d_done, 0));
+    // the previous call's result copy must have left the staging buffers
+    KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_out_free, 0));
     rc = kivi_decode(h, h->st_q, h->st_k, h->st_v, q_per_kv, h->st_out, weights ? h->st_w : nullptr,
                      scale_logits, stream);
     if (rc) return rc;
     KIVI_CUDA(cudaEventRecord(h->ev_in_free, st));
+    // result copy on the cache's own stream, so the next layer's kernels on
+    // `stream` do not queue behind it (kivi_host_join orders `stream` after it)
+    KIVI_CUDA(cudaEventRecord(h->ev_out_ready, st));
+    KIVI_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_out_ready, 0));
     KIVI_CUDA(cudaMemcpyAsync(out, h->st_out, sizeof(float) * U * q_per_kv * d,
-                              cudaMemcpyDeviceToHost, st));
+                              cudaMemcpyDeviceToHost, h->d2h));
     if (weights)
-        KIVI_CUDA(cudaMemcpyAsync(weights, h->st_w, sizeof(float) * wlen, cudaMemcpyDeviceToHost, st));
+        KIVI_CUDA(cudaMemcpyAsync(weights, h->st_w, sizeof(float) * wlen, cudaMemcpyDeviceToHost,
+                                  h->d2h));
+    KIVI_CUDA(cudaEventRecord(h->ev_out_free, h->d2h));
+    return KIVI_OK;
+}
+
+kivi_status kivi_host_join(kivi_cache* h, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (!h->d2h) return KIVI_OK;  // no host-path call yet
+    DeviceGuard g(h->device);
+    KIVI_CUDA(cudaStreamWaitEvent(S(stream), h->ev_out_free, 0));
     return KIVI_OK;
 }
 

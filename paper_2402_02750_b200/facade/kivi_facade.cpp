@@ -482,6 +482,7 @@ DecodeOutput decode_attention(const Matrix& t_Q, const Matrix& t_K, const Matrix
     out.weights = Matrix(1, l);
     check(kivi_decode_host(h, t_Q.data(), t_K.data(), t_V.data(), 1, out.output.data(),
                            out.weights.data(), opts.scale_logits ? 1 : 0, nullptr));
+    check(kivi_host_join(h, nullptr));
     sync();
     store_state(h, key_state, value_state, cfg);
     return out;

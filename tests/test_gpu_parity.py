@@ -378,7 +378,8 @@ def test_host_buffers_path_equals_device_path(cuda):
         q, tk, tv = rnd(rng, U, 1, d), rnd(rng, U, d), rnd(rng, U, d)
         out_h = np.zeros((U, 1, d), np.float32)
         a.decode_host(q, tk, tv, out_h)
-        torch.cuda.synchronize()
+        a.host_join()
+        torch.cuda.current_stream().synchronize()
         out_d = b.decode(dev(q), dev(tk), dev(tv)).cpu().numpy()
         assert out_h.tobytes() == out_d.tobytes()
 
