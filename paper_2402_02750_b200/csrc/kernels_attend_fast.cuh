@@ -129,6 +129,12 @@ struct FastArgs {
     float2* part_ml;    // [units][n_sub]   (max, sum) in log2 domain
     float* wlog;        // [units][l] log2-domain logits, or null
     int* work;          // body kernel: dynamic item counter (zeroed before launch)
+    // fused append (tail kernel only): when l_app >= 0 the tail kernel first
+    // appends token rows tk/tv [units][128] to each unit it owns (the cache
+    // held l_app tokens), then streams that unit's items.
+    const float* tk;
+    const float* tv;
+    int l_app;
 };
 
 // Per-warp shared memory.  One q staging buffer suffices for NSLOT == 2: the
@@ -722,8 +728,28 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     const int tw = gridDim.x * NW;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
 
-    int f_item = gw, f_job = 0;
+    // Item order.  Default: item i to warp i mod tw.  Fused append: a warp owns
+    // whole units (u = gw, gw + tw, ...) and walks each unit's items in order,
+    // appending the unit's new token before issuing its first job.
+    const bool fused = a.l_app >= 0;
+    const int nper = a.n_per_unit;
+    const int n_units = a.n_items / nper;
+    auto first_item = [&]() { return fused ? gw * nper : gw; };
+    auto next_item = [&](int it) {
+        if (!fused) return it + tw;
+        return (it % nper == nper - 1) ? it + 1 + (tw - 1) * nper : it + 1;
+    };
+    auto enter_unit = [&](int it) {  // whole warp
+        if (fused && it < a.n_items && it % nper == 0) {
+            append_unit_fast<B>(a.c, a.tk, a.tv, a.l_app, it / nper, lane);
+            fence_proxy_async_global();  // the unit's TMA reads follow its append
+            __syncwarp();
+        }
+    };
+    (void)n_units;
+    int f_item = first_item(), f_job = 0;
     ItemPlan f_plan{};
+    enter_unit(f_item);
     if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
@@ -733,8 +759,9 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
             issue_job<B>(a, f_plan.u, jd, f_job == 0, wbase + s * SLOT, qraw, &bars[s], policy);
         }
         if (++f_job == f_plan.njobs) {
-            f_item += tw;
+            f_item = next_item(f_item);
             f_job = 0;
+            enter_unit(f_item);
             if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
         }
     };
@@ -754,7 +781,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
         cs ^= 1;
     };
 
-    for (int item = gw; item < a.n_items; item += tw) {
+    for (int item = first_item(); item < a.n_items; item = next_item(item)) {
         const ItemPlan p = plan_item<B>(a, item);
         const int nk = p.nkq + p.nkf;
         for (int j = 0; j < nk; ++j) {

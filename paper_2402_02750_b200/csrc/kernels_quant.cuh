@@ -180,13 +180,14 @@ __device__ __forceinline__ void minmax_pair_reduce8(float& lo, int& ilo, float& 
     }
 }
 
+// One unit's append_token by one warp (d = 128, G = 32).  Also called by the
+// residual-window attend kernel, which appends each unit it owns right before
+// streaming that unit's residual items (kivi_decode's fused route).
 template <int B>
-__global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const float* __restrict__ tk,
-                                                          const float* __restrict__ tv, int64_t l) {
+__device__ __forceinline__ void append_unit_fast(const CacheDev& c, const float* __restrict__ tk,
+                                                 const float* __restrict__ tv, int64_t l,
+                                                 int64_t u, int lane) {
     constexpr int D = 128, G = 32;
-    const int lane = threadIdx.x & 31;
-    const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (u >= c.n_units) return;
     const int R = c.R;
     const int slot = (int)(l % R);
     float* kring = c.kring + u * c.ring_ustride;
@@ -251,6 +252,15 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
             }
         }
     }
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const float* __restrict__ tk,
+                                                          const float* __restrict__ tv, int64_t l) {
+    const int lane = threadIdx.x & 31;
+    const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (u >= c.n_units) return;
+    append_unit_fast<B>(c, tk, tv, l, u, lane);
 }
 
 // ---- materialize (reference materialize_*, kv_cache.cpp:100-106) ---------

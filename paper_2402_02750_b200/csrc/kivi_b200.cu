@@ -308,9 +308,28 @@ int num_sms() {
     return g_num_sms;
 }
 
+// Whether kivi_decode may fold this step's append into the residual-window
+// kernel (the cache holds l tokens; the decision uses the geometry after the
+// append, as launch_fast will).
+bool fused_append_ok(const kivi_cache* h, int q_per_kv) {
+    // off by default: measured C2 8.73 vs 8.49 ms/step (the append lengthens the
+    // residual items, which sit on the critical path); read per call (tests flip it)
+    const int on = env_int("KIVI_FUSED_APPEND", 0);
+    static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
+    const kivi_config& c = h->cfg;
+    if (!on || !tail_side || q_per_kv != 1 || h->attend_path == 1) return false;
+    if (c.head_dim != 128 || c.group_size != 32 || (c.bits != 2 && c.bits != 4)) return false;
+    const int64_t l = h->l + 1, R = c.residual_length;
+    const int64_t vg = l - std::min(l, R);
+    const bool latency_bound =
+        env_int("KIVI_SMALL_ITEMS", 1) && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
+    return !latency_bound && vg > 0 && ((vg - 1) / 32 * 32) / fast::BSUB > 0;
+}
+
 template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
-                        cudaStream_t st) {
+                        cudaStream_t st, const float* tk = nullptr, const float* tv = nullptr,
+                        int64_t l_app = -1) {
     const int64_t U = h->n_units;
     // Items: body = whole BSUB-token sub-chunks below floor32(vg) (all keys and
     // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
@@ -322,7 +341,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // path, so every token goes through tsub-token items instead.
     const int small_items = env_int("KIVI_SMALL_ITEMS", 1);  // read per call (tests flip it)
     const bool latency_bound = small_items && U * ceil_div(h->l, fast::BSUB) < 4 * num_sms();
-    const int64_t nfull = latency_bound ? 0 : ((h->vg() / 32) * 32) / fast::BSUB;
+    // fused append: the body must not cover the token the append pops into the
+    // quantized store (token vg - 1), so it stops at floor32(vg - 1)
+    const int64_t body_vg = l_app >= 0 ? h->vg() - 1 : h->vg();
+    const int64_t nfull = latency_bound ? 0 : ((body_vg / 32) * 32) / fast::BSUB;
+    if (l_app >= 0 && (latency_bound || nfull == 0))
+        return fail(KIVI_ERR_USAGE, "internal: fused append outside its route");
     const int64_t t_first = nfull * fast::BSUB;
     const int tsub = latency_bound ? tsub_small : tsub_env;
     const int64_t n_sub = nfull + ceil_div(h->l - t_first, tsub);
@@ -338,7 +362,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     rc = ensure(&h->stats, &h->stats_cap, U);
     if (rc) return rc;
 
-    fast::FastArgs a;
+    fast::FastArgs a{};
+    a.l_app = -1;
     a.c = h->dev;
     a.l = (int)h->l;
     a.kg = (int)h->kg();
@@ -405,6 +430,9 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.sub = tsub;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
+        a.tk = tk;
+        a.tv = tv;
+        a.l_app = (int)l_app;
         if (nfull > 0 && tail_st != st && tail_warp_ctas) {
             // one-warp CTAs beside the body kernel: every tail item its own warp
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_warp_ctas,
@@ -421,6 +449,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         h->total_launches++;
     }
     if (nfull > 0) {
+        a.l_app = -1;
         a.k_first = 0;
         a.t_first = 0;
         a.sub = fast::BSUB;
@@ -833,13 +862,19 @@ kivi_status kivi_prefill(kivi_cache* h, const float* keys, const float* values, 
     return KIVI_OK;
 }
 
-kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void* stream) {
-    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
-    if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
-    DeviceGuard g(h->device);
-    cudaStream_t st = S(stream);
-    kivi_status rc = ensure_capacity(h, h->l + 1, st);
-    if (rc) return rc;
+// Host-side counters of one append_token (kv_cache.cpp:66-98).
+static void append_bookkeeping(kivi_cache* h) {
+    const int64_t R = h->cfg.residual_length;
+    // residual_capacity = max(capacity, rows after the push) (kv_cache.cpp:78, 93-94)
+    const int64_t krows_after_push = h->l % R + 1;
+    h->kres_cap = std::max(h->kres_cap, krows_after_push);
+    const int64_t vrows = std::min(h->l, R) == R ? R : std::min(h->l, R) + 1;
+    h->vres_cap = std::max(h->vres_cap, vrows);
+    h->l += 1;
+}
+
+static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t_v,
+                                 cudaStream_t st) {
     const kivi_config& cf = h->cfg;
     if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4)) {
         const unsigned grid = (unsigned)ceil_div(h->n_units, 8);
@@ -852,13 +887,19 @@ kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void*
     }
     KIVI_LAUNCHED();
     h->total_launches++;
-    const int64_t R = h->cfg.residual_length;
-    // residual_capacity = max(capacity, rows after the push) (kv_cache.cpp:78, 93-94)
-    const int64_t krows_after_push = h->l % R + 1;
-    h->kres_cap = std::max(h->kres_cap, krows_after_push);
-    const int64_t vrows = std::min(h->l, R) == R ? R : std::min(h->l, R) + 1;
-    h->vres_cap = std::max(h->vres_cap, vrows);
-    h->l += 1;
+    return KIVI_OK;
+}
+
+kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void* stream) {
+    if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
+    DeviceGuard g(h->device);
+    cudaStream_t st = S(stream);
+    kivi_status rc = ensure_capacity(h, h->l + 1, st);
+    if (rc) return rc;
+    rc = append_launch(h, t_k, t_v, st);
+    if (rc) return rc;
+    append_bookkeeping(h);
     return KIVI_OK;
 }
 
@@ -890,6 +931,22 @@ kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
     if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
     if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL query/output");
+    if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
+    if (fused_append_ok(h, q_per_kv) && fast_supported(h, q_per_kv)) {
+        // The append runs inside the residual-window kernel, on each unit right
+        // before its residual items; the body items never read what it writes
+        // (launch_fast stops the body at floor32(vg - 1)).
+        DeviceGuard g(h->device);
+        cudaStream_t st = S(stream);
+        kivi_status rc = ensure_capacity(h, h->l + 1, st);
+        if (rc) return rc;
+        const int64_t l_app = h->l;
+        append_bookkeeping(h);
+        const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
+        const float qscale = scale * fast::LOG2E;
+        if (h->cfg.bits == 2) return launch_fast<2>(h, t_q, out, weights, qscale, st, t_k, t_v, l_app);
+        return launch_fast<4>(h, t_q, out, weights, qscale, st, t_k, t_v, l_app);
+    }
     kivi_status rc = kivi_append(h, t_k, t_v, stream);
     if (rc) return rc;
     return kivi_attend(h, t_q, q_per_kv, out, weights, scale_logits, stream);

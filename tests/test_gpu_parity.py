@@ -227,10 +227,13 @@ def test_decode_fast_vs_reference(cuda, bits, l0, small_items, monkeypatch):
     assert e_w <= 1e-5, e_w
 
 
-@pytest.mark.parametrize("small_items", ["0", "1"])
+@pytest.mark.parametrize("route", [("0", "1"), ("0", "0"), ("1", "1")])
 @pytest.mark.parametrize("bits", [2, 4])
-def test_decode_fast_across_flush_and_long_context(cuda, bits, small_items, monkeypatch):
-    monkeypatch.setenv("KIVI_SMALL_ITEMS", small_items)
+def test_decode_fast_across_flush_and_long_context(cuda, bits, route, monkeypatch):
+    # (small items, fused append): the fused route appends inside the
+    # residual-window kernel, across 130 value pops and a key flush
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", route[0])
+    monkeypatch.setenv("KIVI_FUSED_APPEND", route[1])
     cfg = (bits, 32, 128, 128)
     # 130 steps cross a key flush and 130 value pops; ctx ~4k like config 1.
     e_out, _ = run_decode(cfg, U=2, l0=3968, steps=130, path="fast", seed=7, weights=False)
