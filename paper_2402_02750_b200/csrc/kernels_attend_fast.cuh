@@ -135,7 +135,56 @@ struct FastArgs {
     const float* tk;
     const float* tv;
     int l_app;
+    // single-launch decode (few units, tail kernel only; gbar != null): every
+    // warp < n_units appends its unit, a grid-wide counter barrier (cooperative
+    // launch: all CTAs resident) orders the appends before any item, and the
+    // warp that writes a unit's last partial merges the unit (combine_kernel's
+    // arithmetic).  Counters are cumulative over launches: targets are passed.
+    unsigned long long* gbar;
+    unsigned long long gbar_target;
+    unsigned int* unit_done;
+    unsigned int unit_target;
+    float* out;
+    float2* stats;
 };
+
+// Merge unit u's n_sub partials (LSE rescale, log2 domain) by one warp: lane
+// owns channels 4*lane .. 4*lane+3.  Same arithmetic as combine_kernel.  The
+// partial weights are computed once by their owner lane (k mod 32) and
+// broadcast; the partial loads are independent and unrolled so they overlap.
+__device__ __forceinline__ void combine_unit_warp(const float* __restrict__ part_o,
+                                                  const float2* __restrict__ part_ml, int n_sub,
+                                                  int64_t u, float* __restrict__ out,
+                                                  float2* __restrict__ stats, int lane) {
+    const float2* ml = part_ml + u * n_sub;
+    const float4* po = reinterpret_cast<const float4*>(part_o + u * n_sub * D) + lane;
+    float M = -INFINITY;
+    for (int k = lane; k < n_sub; k += 32) M = fmaxf(M, __ldcg(&ml[k]).x);
+    M = warp_max_redux(M);
+    float L = 0.f;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < n_sub; k0 += 32) {
+        float w = 0.f;
+        if (k0 + lane < n_sub) {
+            const float2 m = __ldcg(&ml[k0 + lane]);
+            w = exp2f(m.x - M);
+            L = fmaf(m.y, w, L);
+        }
+        const int nk = min(32, n_sub - k0);
+#pragma unroll 8
+        for (int i = 0; i < nk; ++i) {
+            const float wi = __shfl_sync(0xffffffffu, w, i);
+            const float4 p = __ldcg(po + (int64_t)(k0 + i) * (D / 4));
+            o.x = fmaf(p.x, wi, o.x);
+            o.y = fmaf(p.y, wi, o.y);
+            o.z = fmaf(p.z, wi, o.z);
+            o.w = fmaf(p.w, wi, o.w);
+        }
+    }
+    L = warp_sum(L);
+    reinterpret_cast<float4*>(out + u * D)[lane] = make_float4(o.x / L, o.y / L, o.z / L, o.w / L);
+    if (stats && lane == 0) stats[u] = make_float2(M, L);
+}
 
 // Per-warp shared memory.  One q staging buffer suffices for NSLOT == 2: the
 // next item's first job is issued only after the current item's job 0 (which
@@ -731,7 +780,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     // Item order.  Default: item i to warp i mod tw.  Fused append: a warp owns
     // whole units (u = gw, gw + tw, ...) and walks each unit's items in order,
     // appending the unit's new token before issuing its first job.
-    const bool fused = a.l_app >= 0;
+    const bool fused = a.l_app >= 0 && !a.gbar;
     const int nper = a.n_per_unit;
     const int n_units = a.n_items / nper;
     auto first_item = [&]() { return fused ? gw * nper : gw; };
@@ -747,9 +796,24 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
         }
     };
     (void)n_units;
+    if (a.gbar) {
+        // single-launch decode: appends, then a grid-wide barrier
+        if (gw < n_units) {
+            append_unit_fast<B>(a.c, a.tk, a.tv, a.l_app, gw, lane);
+            fence_proxy_async_global();
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            atomicAdd(a.gbar, 1ull);
+            while (ld_acquire_u64(a.gbar) < a.gbar_target) __nanosleep(100);
+        }
+        __syncwarp();
+        fence_proxy_async_global();  // this warp's TMA reads follow every append
+    }
     int f_item = first_item(), f_job = 0;
     ItemPlan f_plan{};
-    enter_unit(f_item);
+    if (!a.gbar) enter_unit(f_item);
     if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
@@ -813,28 +877,103 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
                 const int64_t pi = (int64_t)p.u * a.n_sub + p.k;
                 v_finalize<B>(slot, vacc, zacc0, zacc1, facc, ml, a.part_o + pi * D,
                               a.part_ml + pi, lane);
+                if (a.gbar) {
+                    // the unit's last partial merges the unit
+                    __threadfence();
+                    __syncwarp();
+                    unsigned int done = 0;
+                    if (lane == 0) done = atomicAdd(&a.unit_done[p.u], 1u) + 1u;
+                    done = __shfl_sync(0xffffffffu, done, 0);
+                    if (done == a.unit_target) {
+                        __threadfence();
+                        combine_unit_warp(a.part_o, a.part_ml, a.n_sub, p.u, a.out, a.stats, lane);
+                    }
+                }
             }
             release_slot();
         }
     }
 }
 
-// K5: merge the per-item partials of every unit (LSE rescale in log2 domain).
-__global__ void combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                               int n_sub, float* __restrict__ out, float2* __restrict__ stats) {
-    const int64_t u = blockIdx.x;
-    const int c = threadIdx.x;  // 128 threads
+// K5 row merge, one 128-thread block per output row (thread c = channel c):
+// partial k of the row is part_ml[ml0 + k * ms] / part_o[(ml0 + k * ms) * D].
+// The max and the weights are computed in parallel over k (128 partials per
+// pass), then every thread streams its channel of the partials with
+// independent loads — the loop carries no exp2 and no load latency chain.
+__device__ __forceinline__ void combine_row(const float* __restrict__ part_o,
+                                            const float2* __restrict__ part_ml, int n_sub,
+                                            int64_t ml0, int ms, float* __restrict__ out_row,
+                                            float2* __restrict__ stat) {
+    __shared__ float sw[128];
+    __shared__ float sred[8];
+    const int c = threadIdx.x, warp = c >> 5, lane = c & 31;
+    float m = -INFINITY;
+    for (int k = c; k < n_sub; k += 128) m = fmaxf(m, part_ml[ml0 + (int64_t)k * ms].x);
+    m = warp_max_redux(m);
+    if (lane == 0) sred[warp] = m;
+    __syncthreads();
+    const float M = fmaxf(fmaxf(sred[0], sred[1]), fmaxf(sred[2], sred[3]));
+    float Lp = 0.f, o = 0.f, o1 = 0.f;
+    for (int k0 = 0; k0 < n_sub; k0 += 128) {
+        __syncthreads();  // sw reuse (and sred reads above)
+        if (k0 + c < n_sub) {
+            const float2 ml = part_ml[ml0 + (int64_t)(k0 + c) * ms];
+            const float w = exp2f(ml.x - M);
+            sw[c] = w;
+            Lp = fmaf(ml.y, w, Lp);
+        }
+        __syncthreads();
+        const int nk = min(128, n_sub - k0);
+        int i = 0;
+#pragma unroll 4
+        for (; i + 1 < nk; i += 2) {
+            o = fmaf(part_o[(ml0 + (int64_t)(k0 + i) * ms) * D + c], sw[i], o);
+            o1 = fmaf(part_o[(ml0 + (int64_t)(k0 + i + 1) * ms) * D + c], sw[i + 1], o1);
+        }
+        if (i < nk) o = fmaf(part_o[(ml0 + (int64_t)(k0 + i) * ms) * D + c], sw[i], o);
+    }
+    Lp = warp_sum(Lp);
+    __syncthreads();
+    if (lane == 0) sred[4 + warp] = Lp;
+    __syncthreads();
+    const float L = (sred[4] + sred[5]) + (sred[6] + sred[7]);
+    out_row[c] = (o + o1) / L;
+    if (stat && c == 0) *stat = make_float2(M, L);
+}
+
+// The same merge as one serial loop per thread: better when there are many
+// rows (thousands of blocks hide each block's latency chain; measured C3 20.5
+// vs 28.5 us), worse when there are few (C1: 12.8 vs 7.4 us).
+__device__ __forceinline__ void combine_row_serial(const float* __restrict__ part_o,
+                                                   const float2* __restrict__ part_ml, int n_sub,
+                                                   int64_t ml0, int ms, float* __restrict__ out_row,
+                                                   float2* __restrict__ stat) {
+    const int c = threadIdx.x;
     float M = -INFINITY;
-    for (int k = 0; k < n_sub; ++k) M = fmaxf(M, part_ml[u * n_sub + k].x);
+    for (int k = 0; k < n_sub; ++k) M = fmaxf(M, part_ml[ml0 + (int64_t)k * ms].x);
     float L = 0.f, o = 0.f;
     for (int k = 0; k < n_sub; ++k) {
-        const float2 ml = part_ml[u * n_sub + k];
+        const int64_t pi = ml0 + (int64_t)k * ms;
+        const float2 ml = part_ml[pi];
         const float w = exp2f(ml.x - M);
         L = fmaf(ml.y, w, L);
-        o = fmaf(part_o[(u * n_sub + k) * D + c], w, o);
+        o = fmaf(part_o[pi * D + c], w, o);
     }
-    out[u * D + c] = o / L;
-    if (stats && c == 0) stats[u] = make_float2(M, L);
+    out_row[c] = o / L;
+    if (stat && c == 0) *stat = make_float2(M, L);
+}
+
+// K5: merge the per-item partials of every unit (LSE rescale in log2 domain).
+__global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ part_o,
+                                                      const float2* __restrict__ part_ml, int n_sub,
+                                                      float* __restrict__ out,
+                                                      float2* __restrict__ stats, int parallel) {
+    const int64_t u = blockIdx.x;
+    if (parallel)
+        combine_row(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D, stats ? stats + u : nullptr);
+    else
+        combine_row_serial(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D,
+                           stats ? stats + u : nullptr);
 }
 
 // Optional weights: w_t = 2^(logit2_t - M) / L, in place over the wlog buffer.

@@ -493,24 +493,20 @@ __global__ void __launch_bounds__(NW * 32, 2) attend_gqa_kernel(fast::FastArgs a
 }
 
 // K5 for H heads: rows r = u*H + h; partial (u, k, h) at (u*n_sub + k)*H + h.
-__global__ void combine_heads_kernel(const float* __restrict__ part_o,
-                                     const float2* __restrict__ part_ml, int n_sub, int H,
-                                     float* __restrict__ out, float2* __restrict__ stats) {
+__global__ void __launch_bounds__(128) combine_heads_kernel(const float* __restrict__ part_o,
+                                                            const float2* __restrict__ part_ml,
+                                                            int n_sub, int H,
+                                                            float* __restrict__ out,
+                                                            float2* __restrict__ stats,
+                                                            int parallel) {
     const int64_t r = blockIdx.x;
     const int64_t u = r / H, h = r % H;
-    const int c = threadIdx.x;
-    float M = -INFINITY;
-    for (int k = 0; k < n_sub; ++k) M = fmaxf(M, part_ml[(u * n_sub + k) * H + h].x);
-    float L = 0.f, o = 0.f;
-    for (int k = 0; k < n_sub; ++k) {
-        const int64_t pi = (u * n_sub + k) * H + h;
-        const float2 ml = part_ml[pi];
-        const float w = exp2f(ml.x - M);
-        L = fmaf(ml.y, w, L);
-        o = fmaf(part_o[pi * D + c], w, o);
-    }
-    out[r * D + c] = o / L;
-    if (stats && c == 0) stats[r] = make_float2(M, L);
+    if (parallel)
+        fast::combine_row(part_o, part_ml, n_sub, u * n_sub * H + h, H, out + r * D,
+                          stats ? stats + r : nullptr);
+    else
+        fast::combine_row_serial(part_o, part_ml, n_sub, u * n_sub * H + h, H, out + r * D,
+                                 stats ? stats + r : nullptr);
 }
 
 }  // namespace gqa

@@ -132,6 +132,9 @@ struct kivi_cache {
     int* work = nullptr;  // body kernel dynamic item counter
     cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
     cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
+    unsigned long long* small_sync = nullptr;  // [1 + n_units] single-launch decode counters
+    unsigned long long small_gbar = 0;         // cumulative grid-barrier target
+    unsigned int small_units = 0;              // cumulative per-unit item target
     cudaStream_t d2h = nullptr;         // result copies of the host path
     cudaEvent_t ev_out_ready = nullptr; // staged result written by the kernels
     cudaEvent_t ev_out_free = nullptr;  // staged result copied to the host
@@ -326,6 +329,102 @@ bool fused_append_ok(const kivi_cache* h, int q_per_kv) {
     return !latency_bound && vg > 0 && ((vg - 1) / 32 * 32) / fast::BSUB > 0;
 }
 
+// Few units (the latency-bound route): one cooperative launch appends,
+// attends and merges (no append / combine launches).
+bool small_fused_ok(const kivi_cache* h, int q_per_kv) {
+    const kivi_config& c = h->cfg;
+    // off by default: measured slower on C1 (51.6 vs 22.1 + append + combine us):
+    // the grid barrier and the last-warp merges serialise latency-bound phases
+    if (!env_int("KIVI_SMALL_FUSED", 0) || q_per_kv != 1 || h->attend_path == 1) return false;
+    if (c.head_dim != 128 || c.group_size != 32 || (c.bits != 2 && c.bits != 4)) return false;
+    const int64_t l = h->l + 1;
+    return env_int("KIVI_SMALL_ITEMS", 1) && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
+}
+
+template <int B>
+kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, const float* tv,
+                               float* out, float* weights, float qscale, int64_t l_app,
+                               cudaStream_t st) {
+    const int64_t U = h->n_units;
+    static const int tsub = std::max(32, std::min(fast::SUB, env_int("KIVI_SMALL_SUB", 64)) / 32 * 32);
+    const int64_t n_sub = ceil_div(h->l, tsub);
+    if (h->l >= (1LL << 30) || U * n_sub >= (1LL << 30))
+        return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, tsub) + 2);
+    kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
+    if (rc) return rc;
+    rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap);
+    if (rc) return rc;
+    rc = ensure(&h->stats, &h->stats_cap, U);
+    if (rc) return rc;
+    if (!h->small_sync) {
+        KIVI_CUDA(dalloc(&h->small_sync, (size_t)(1 + U)));
+        KIVI_CUDA(cudaMemsetAsync(h->small_sync, 0, sizeof(unsigned long long) * (1 + U), st));
+    }
+    const int smem = fast::WS2::STRIDE * fast::WARPS;
+    static int per_sm = 0;
+    if (!per_sm) {
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    fast::FastArgs a{};
+    a.c = h->dev;
+    a.l = (int)h->l;
+    a.kg = (int)h->kg();
+    a.vg = (int)h->vg();
+    a.n_sub = (int)n_sub;
+    a.k_first = 0;
+    a.t_first = 0;
+    a.sub = tsub;
+    a.n_per_unit = (int)n_sub;
+    a.n_items = (int)(U * n_sub);
+    a.q = q;
+    a.qscale = qscale;
+    a.part_o = h->part_o;
+    a.part_ml = h->part_ml;
+    a.wlog = weights;
+    a.tk = tk;
+    a.tv = tv;
+    a.l_app = (int)l_app;
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
+                                           std::max<int64_t>(ceil_div(a.n_items, fast::WARPS),
+                                                             ceil_div(U, fast::WARPS)));
+    h->small_gbar += (unsigned long long)(grid * fast::WARPS);
+    h->small_units += (unsigned int)n_sub;
+    a.gbar = h->small_sync;
+    a.gbar_target = h->small_gbar;
+    a.unit_done = reinterpret_cast<unsigned int*>(h->small_sync + 1);
+    a.unit_target = h->small_units;
+    a.out = out;
+    a.stats = weights ? h->stats : nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profile) {
+        e0 = h->take_event();
+        e1 = h->take_event();
+        cudaEventRecord(e0, st);
+    }
+    void* args[] = {&a};
+    KIVI_CUDA(cudaLaunchCooperativeKernel((const void*)fast::attend_tail_kernel<B>, dim3((unsigned)grid),
+                                          dim3(fast::WARPS * 32), args, (size_t)smem, st));
+    KIVI_LAUNCHED();
+    if (h->profile) {
+        cudaEventRecord(e1, st);
+        h->events.emplace_back(e0, e1);
+    }
+    h->main_launches++;
+    h->total_launches++;
+    if (weights) {
+        fast::normalize_weights_kernel<<<grid_for(U * h->l), 256, 0, st>>>(weights, h->stats, h->l,
+                                                                            U);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    return KIVI_OK;
+}
+
 template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st, const float* tk = nullptr, const float* tv = nullptr,
@@ -480,7 +579,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // K5: merge the per-item partials (a separate launch keeps the merge work
     // balanced; fusing it into the attend tail serialised it on the last warps)
     fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
-                                                          weights ? h->stats : nullptr);
+                                                          weights ? h->stats : nullptr,
+                                                          U < 4 * num_sms());
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
@@ -600,7 +700,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     }
     h->main_launches++;
     gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
-        h->part_o, h->part_ml, (int)n_sub, H, out, weights ? h->stats : nullptr);
+        h->part_o, h->part_ml, (int)n_sub, H, out, weights ? h->stats : nullptr,
+        U * H < 4 * num_sms());
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
@@ -705,6 +806,7 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     cudaFree(h->work);
+    if (h->small_sync) cudaFree(h->small_sync);
     if (h->d2h) cudaStreamDestroy(h->d2h);
     if (h->ev_out_ready) cudaEventDestroy(h->ev_out_ready);
     if (h->ev_out_free) cudaEventDestroy(h->ev_out_free);
@@ -932,6 +1034,19 @@ kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const
     if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
     if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL query/output");
     if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
+    if (small_fused_ok(h, q_per_kv) && fast_supported(h, q_per_kv)) {
+        DeviceGuard g(h->device);
+        cudaStream_t st = S(stream);
+        kivi_status rc = ensure_capacity(h, h->l + 1, st);
+        if (rc) return rc;
+        const int64_t l_app = h->l;
+        append_bookkeeping(h);
+        const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
+        const float qscale = scale * fast::LOG2E;
+        if (h->cfg.bits == 2)
+            return launch_small_fused<2>(h, t_q, t_k, t_v, out, weights, qscale, l_app, st);
+        return launch_small_fused<4>(h, t_q, t_k, t_v, out, weights, qscale, l_app, st);
+    }
     if (fused_append_ok(h, q_per_kv) && fast_supported(h, q_per_kv)) {
         // The append runs inside the residual-window kernel, on each unit right
         // before its residual items; the body items never read what it writes

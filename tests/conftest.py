@@ -16,6 +16,7 @@ if TESTS not in sys.path:
 # so they pin the body + tail split by default; the small-item route has its
 # own parametrised cases (test_gpu_parity.py, item_policy).
 os.environ.setdefault("KIVI_SMALL_ITEMS", "0")
+os.environ.setdefault("KIVI_SMALL_FUSED", "0")
 
 
 def pytest_configure(config):

@@ -215,25 +215,33 @@ def test_decode_generic_vs_reference(cuda, cfg, l0):
     assert e_w <= 1e-6, e_w
 
 
-@pytest.mark.parametrize("small_items", ["0", "1"])
+ROUTES = {"body": ("0", "0"), "small": ("1", "0"), "small_fused": ("1", "1")}
+
+
+@pytest.mark.parametrize("route", sorted(ROUTES))
 @pytest.mark.parametrize("bits", [2, 4])
 @pytest.mark.parametrize("l0", [1, 31, 127, 128, 129, 255, 256, 257, 383, 600, 1153])
-def test_decode_fast_vs_reference(cuda, bits, l0, small_items, monkeypatch):
-    # small_items=1: every token through 64-token items (few-unit route)
-    monkeypatch.setenv("KIVI_SMALL_ITEMS", small_items)
+def test_decode_fast_vs_reference(cuda, bits, l0, route, monkeypatch):
+    # body: body + residual kernels; small: every token through 64-token items
+    # (few-unit route); small_fused: the same in one cooperative launch that
+    # also appends and merges
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", ROUTES[route][0])
+    monkeypatch.setenv("KIVI_SMALL_FUSED", ROUTES[route][1])
     cfg = (bits, 32, 128, 128)
     e_out, e_w = run_decode(cfg, U=3, l0=l0, steps=4, path="fast", seed=l0 + bits)
     assert e_out <= 1e-5, e_out
     assert e_w <= 1e-5, e_w
 
 
-@pytest.mark.parametrize("route", [("0", "1"), ("0", "0"), ("1", "1")])
+@pytest.mark.parametrize("route", [("0", "1", "0"), ("0", "0", "0"), ("1", "0", "0"),
+                                   ("1", "0", "1")])
 @pytest.mark.parametrize("bits", [2, 4])
 def test_decode_fast_across_flush_and_long_context(cuda, bits, route, monkeypatch):
-    # (small items, fused append): the fused route appends inside the
-    # residual-window kernel, across 130 value pops and a key flush
+    # (small items, fused append, single-launch small route) across 130 value
+    # pops and a key flush: the fused routes append inside the attend launch
     monkeypatch.setenv("KIVI_SMALL_ITEMS", route[0])
     monkeypatch.setenv("KIVI_FUSED_APPEND", route[1])
+    monkeypatch.setenv("KIVI_SMALL_FUSED", route[2])
     cfg = (bits, 32, 128, 128)
     # 130 steps cross a key flush and 130 value pops; ctx ~4k like config 1.
     e_out, _ = run_decode(cfg, U=2, l0=3968, steps=130, path="fast", seed=7, weights=False)
