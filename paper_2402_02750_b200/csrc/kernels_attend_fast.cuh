@@ -56,6 +56,21 @@ constexpr float LOG2E = 1.4426950408889634f;
 #endif
 constexpr int KQ_UNROLL = KIVI_KQ_UNROLL;
 
+// w >> K on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF): the body
+// kernel is ALU-bound on the code extraction, the FMA pipe has headroom.
+#ifndef KIVI_SHR_FMA
+#define KIVI_SHR_FMA 1
+#endif
+template <int K>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t w) {
+#if KIVI_SHR_FMA
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(1u << (32 - K)));
+    return r;
+#else
+    return w >> K;
+#endif
+}
 template <int B>
 struct P;
 template <>
@@ -72,7 +87,7 @@ struct P<2> {
     // acc[0..7] (+)= M * codes of w (codes 2j, 2j+1 in acc[j])
     static __device__ __forceinline__ void fma_word(float2* acc, uint32_t w, float M) {
         const float2 m2 = make_float2(M, M);
-        const uint32_t s = w >> 10;
+        const uint32_t s = shr_fma<10>(w);
         acc[0] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0x3u), KIVI_F(w & 0xCu)), acc[0]);
         acc[1] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0x30u), KIVI_F(w & 0xC0u)), acc[1]);
         acc[2] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0x300u), KIVI_F(w & 0xC00u)), acc[2]);
@@ -95,7 +110,7 @@ struct P<4> {
     static __host__ __device__ constexpr int epos(int k) { return k <= 4 ? 4 * k : 4 * k - 12; }
     static __device__ __forceinline__ void fma_word(float2* acc, uint32_t w, float M) {
         const float2 m2 = make_float2(M, M);
-        const uint32_t s = w >> 12;
+        const uint32_t s = shr_fma<12>(w);
         acc[0] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0xFu), KIVI_F(w & 0xF0u)), acc[0]);
         acc[1] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0xF00u), KIVI_F(w & 0xF000u)), acc[1]);
         acc[2] = __ffma2_rn(m2, make_float2(KIVI_F(w & 0xF0000u), KIVI_F(s & 0xF00u)), acc[2]);
