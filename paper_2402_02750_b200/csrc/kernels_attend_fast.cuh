@@ -144,6 +144,8 @@ struct FastArgs {
     float2* part_ml;    // [units][n_sub]   (max, sum) in log2 domain
     float* wlog;        // [units][l] log2-domain logits, or null
     int* work;          // body kernel: dynamic item counter (zeroed before launch)
+    int body_end;       // tensor-core GQA body: tokens it covers (multiple of 32;
+                        // its last item per unit may be partial)
     // fused append (tail kernel only): when l_app >= 0 the tail kernel first
     // appends token rows tk/tv [units][128] to each unit it owns (the cache
     // held l_app tokens), then streams that unit's items.

@@ -178,7 +178,7 @@ __device__ __forceinline__ void mma_f16_x2(float4& d0, float4& d1, const CodeQua
 template <int H>
 __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[H][2], float qmax,
                                         float* probs, int tok0, uint8_t* bf, float* biasm, int lane,
-                                        uint32_t sel) {
+                                        uint32_t sel, int ntl) {
     const int g = lane >> 2, t = lane & 3;
     const float4* pairs4 = reinterpret_cast<const float4*>(slot + KT * 1024);
     // pre-pass over this lane's channels 4L..4L+3 of the KT tiles: spans,
@@ -186,18 +186,23 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     float dmax = 0.f;
 #pragma unroll
     for (int T = 0; T < KT; ++T) {
-        const float4 p01 = pairs4[T * 64 + 2 * lane];
-        const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
-        const float lo[4] = {p01.x, p01.z, p23.x, p23.z};
-        dmax = fmaxf(dmax, fmaxf(fmaxf(p01.y - p01.x, p01.w - p01.z),
-                                 fmaxf(p23.y - p23.x, p23.w - p23.z)));
+        if (T < ntl) {  // tiles past a partial item's end were not loaded
+            const float4 p01 = pairs4[T * 64 + 2 * lane];
+            const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
+            const float lo[4] = {p01.x, p01.z, p23.x, p23.z};
+            dmax = fmaxf(dmax, fmaxf(fmaxf(p01.y - p01.x, p01.w - p01.z),
+                                     fmaxf(p23.y - p23.x, p23.w - p23.z)));
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-            float b = qv[h][0].x * lo[0];
-            b = fmaf(qv[h][0].y, lo[1], b);
-            b = fmaf(qv[h][1].x, lo[2], b);
-            b = fmaf(qv[h][1].y, lo[3], b);
-            biasm[lane * BIAS_ROW + T * H + h] = b;
+            for (int h = 0; h < H; ++h) {
+                float b = qv[h][0].x * lo[0];
+                b = fmaf(qv[h][0].y, lo[1], b);
+                b = fmaf(qv[h][1].x, lo[2], b);
+                b = fmaf(qv[h][1].y, lo[3], b);
+                biasm[lane * BIAS_ROW + T * H + h] = b;
+            }
+        } else {
+#pragma unroll
+            for (int h = 0; h < H; ++h) biasm[lane * BIAS_ROW + T * H + h] = 0.f;
         }
     }
     dmax = warp_max_redux(dmax);
@@ -268,7 +273,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     // the barrier of tile T).  Building tile T+1 during tile T's MMAs measured
     // slower (374 vs 360 us on C3): register pressure, no extra overlap.
 #pragma unroll 1
-    for (int T = 0; T < KT; ++T) {
+    for (int T = 0; T < ntl; ++T) {
         produce(T);
         __syncwarp();
         consume(T);
@@ -281,7 +286,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
 // pair blocks L + 32i (tokens tb, tb+4 with tb = (b >> 2) * 8 + (b & 3)).
 template <int H>
 __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t wstride, float2* ml,
-                                              int lane) {
+                                              int lane, int ntok = SUB) {
     __syncwarp();
     float2 v[4][H];
 #pragma unroll
@@ -314,8 +319,8 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
             const int tb = (b >> 2) * 8 + (b & 3);
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                wlog[h * wstride + tb] = v[i][h].x;
-                wlog[h * wstride + tb + 4] = v[i][h].y;
+                if (tb < ntok) wlog[h * wstride + tb] = v[i][h].x;
+                if (tb + 4 < ntok) wlog[h * wstride + tb + 4] = v[i][h].y;
             }
         }
     }
@@ -351,15 +356,17 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
 template <int H>
 __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_src, float4 (&vacc)[4][2],
                                           float2 (&zs)[H], int& eb_run, bool first, uint8_t* bf,
-                                          int lane, uint32_t sel) {
+                                          int lane, uint32_t sel, int ntok = VT) {
     const int g = lane >> 2, t = lane & 3;
     const float4* pairs4 = reinterpret_cast<const float4*>(slot + VT * 32);
     const float2* pairs2 = reinterpret_cast<const float2*>(slot + VT * 32);
     float dmax = 0.f;
 #pragma unroll
     for (int i = 0; i < VT / 16; ++i) {
-        const float4 pr = pairs4[lane + 32 * i];
-        dmax = fmaxf(dmax, fmaxf(pr.y - pr.x, pr.w - pr.z));
+        if ((lane + 32 * i) / 2 < ntok) {  // float4 f holds token f / 2
+            const float4 pr = pairs4[lane + 32 * i];
+            dmax = fmaxf(dmax, fmaxf(pr.y - pr.x, pr.w - pr.z));
+        }
     }
     dmax = warp_max_redux(dmax);
     const int eb = exp_byte(dmax * (1.0f / 3.0f));
@@ -383,7 +390,10 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
     auto produce = [&](int s) {
         uint32_t* bv = reinterpret_cast<uint32_t*>(bf) + (s & 1) * (4 * BFV_CG);
         const int ta = 16 * s + toff, tb = ta + 4;
-        const float2 pa = pairs2[ta * 4 + cgp], pb = pairs2[tb * 4 + cgp];
+        // tokens past a partial item's end: zero operands (their slot bytes
+        // were not loaded)
+        const float2 pa = ta < ntok ? pairs2[ta * 4 + cgp] : make_float2(0.f, 0.f);
+        const float2 pb = tb < ntok ? pairs2[tb * 4 + cgp] : make_float2(0.f, 0.f);
         const float2 d2 = __fmul2_rn(make_float2(pa.y - pa.x, pb.y - pb.x), make_float2(f, f));
         const float2 z2 = make_float2(pa.x, pb.x);
         float2 P[H];  // (p_h[ta], p_h[tb])
@@ -426,7 +436,7 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
     };
     // one warp barrier per K step (two buffers, as in key_job)
 #pragma unroll 1
-    for (int s = 0; s < VT / 16; ++s) {
+    for (int s = 0; s < (ntok + 15) / 16; ++s) {
         produce(s);
         __syncwarp();
         consume(s);
@@ -474,9 +484,12 @@ __device__ __forceinline__ void value_finalize(const float4 (&vacc)[4][2], const
 }
 
 // -------------------------------------------------------------------------
-// Body kernel: persistent warps take items (unit, fully quantized 256-token
-// sub-chunk) from an atomic counter; 2 key jobs + 2 value jobs per item,
-// streamed through two TMA slots per warp (as fast::attend_body_kernel).
+// Body kernel: persistent warps take items (unit, 256-token sub-chunk of
+// [0, body_end) — all keys and values quantized; the last item of a unit may
+// be partial) from an atomic counter; key and value jobs stream through two TMA
+// slots per warp (as fast::attend_body_kernel).  A partial item's missing
+// tiles / tokens are never loaded nor computed: zero-byte jobs complete their
+// barrier at once, their logits are -inf and their value operands zero.
 // -------------------------------------------------------------------------
 template <int H>
 __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fast::FastArgs a) {
@@ -518,27 +531,35 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             uint8_t* slot = wbase + s * SLOT;
             uint64_t* bar = &bars[s];
             const int kk = a.k_first + f_k;
+            const int Ti = min(SUB, a.body_end - f_k * SUB);  // item tokens (partial last item)
             fence_proxy_async_smem();
             if (f_job < NKJ) {
+                const int ntl = min(KT, max(0, Ti / 32 - f_job * KT));
                 const int64_t tile0 = (int64_t)kk * (SUB / 32) + f_job * KT;
-                constexpr uint32_t cb = KT * PB::TILE_CODE;
-                constexpr uint32_t pb = KT * D * 8;
+                const uint32_t cb = (uint32_t)ntl * PB::TILE_CODE;
+                const uint32_t pb = (uint32_t)ntl * D * 8;
                 constexpr uint32_t qb = H * D * 4;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? qb : 0));
-                bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE, cb,
-                                     bar, policy);
-                bulk_g2s_evict_first(slot + cb, c.kpairs + f_u * c.kp_ustride + tile0 * D, pb, bar,
-                                     policy);
+                if (ntl) {
+                    bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE,
+                                         cb, bar, policy);
+                    bulk_g2s_evict_first(slot + KT * PB::TILE_CODE,
+                                         c.kpairs + f_u * c.kp_ustride + tile0 * D, pb, bar, policy);
+                }
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * H * D, qb, bar);
             } else {
+                const int ntok = min(VT, max(0, Ti - (f_job - NKJ) * VT));
                 const int64_t ts = (int64_t)kk * SUB + (f_job - NKJ) * VT;
-                constexpr uint32_t cb = VT * PB::TOK_CODE;
-                constexpr uint32_t pb = VT * (D / fast::G) * 8;
+                const uint32_t cb = (uint32_t)ntok * PB::TOK_CODE;
+                const uint32_t pb = (uint32_t)ntok * (D / fast::G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
-                bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb, bar,
-                                     policy);
-                bulk_g2s_evict_first(slot + cb, c.vpairs + f_u * c.vp_ustride + ts * (D / fast::G),
-                                     pb, bar, policy);
+                if (ntok) {
+                    bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb,
+                                         bar, policy);
+                    bulk_g2s_evict_first(slot + VT * PB::TOK_CODE,
+                                         c.vpairs + f_u * c.vp_ustride + ts * (D / fast::G), pb, bar,
+                                         policy);
+                }
             }
         }
         if (++f_job == NJ) {
@@ -569,6 +590,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     for (int item = c_next; item < a.n_items; item = c_next) {
         const int u = item / nper;
         const int k = a.k_first + (item - u * nper);
+        const int Ti = min(SUB, a.body_end - (item - u * nper) * SUB);
         float2 qv[H][2];
         float qmax = 0.f;
 #pragma unroll 1
@@ -587,12 +609,19 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
                 qmax = warp_max_redux(qmax);
                 __syncwarp();  // qraw is reused as the bias scratch below
             }
-            key_job<H>(slot, qv, qmax, probs, jk * KT * 32, bf, biasm, lane, sel);
+            const int ntl = min(KT, max(0, Ti / 32 - jk * KT));
+            if (ntl) key_job<H>(slot, qv, qmax, probs, jk * KT * 32, bf, biasm, lane, sel, ntl);
             release_slot();
+        }
+        if (Ti < SUB) {  // partial item: tokens past its end get zero probability
+            for (int i = lane; i < (SUB - Ti) * H; i += 32) {
+                const int t = Ti + i / H;
+                probs[pidx<H>(t, i % H)] = -INFINITY;
+            }
         }
         float2 ml[H];
         softmax_heads<H>(probs, a.wlog ? a.wlog + (int64_t)u * H * a.l + (int64_t)k * SUB : nullptr,
-                         a.l, ml, lane);
+                         a.l, ml, lane, Ti);
         float4 vacc[4][2];
 #pragma unroll
         for (int cg = 0; cg < 4; ++cg)
@@ -605,7 +634,10 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
 #pragma unroll 1
         for (int jv = 0; jv < NVJ; ++jv) {
             uint8_t* slot = wait_slot();
-            value_job<H>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane, sel);
+            const int ntok = min(VT, max(0, Ti - jv * VT));
+            if (ntok)
+                value_job<H>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane, sel,
+                             ntok);
             if (jv == NVJ - 1) {
                 const int64_t pi = ((int64_t)u * a.n_sub + k) * H;
                 value_finalize<H>(vacc, zs, eb_run, ml, zsm, a.part_o + pi * D, a.part_ml + pi, lane);

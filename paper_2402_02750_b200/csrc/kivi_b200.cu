@@ -601,10 +601,16 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "GQA attend path: cache too large for 32-bit indexing");
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
-    // tensor-core body = whole 256-token sub-chunks below floor32(vg)
     static const int use_tc = env_int("KIVI_GQA_TC", 1);
-    const int64_t nfull = use_tc ? ((h->vg() / 32) * 32) / fast::SUB : 0;
-    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB));
+    // body = [0, floor32(vg)) (partial last item): the CUDA-core residual items
+    // then hold fewer than 32 quantized values
+    static const int partial = env_int("KIVI_GQA_PARTIAL", 1);
+    const int64_t body_end =
+        use_tc ? (partial ? (h->vg() / 32) * 32 : (h->vg() / 32 * 32) / fast::SUB * fast::SUB) : 0;
+    const int64_t nfull = ceil_div(body_end, fast::SUB);
+    const int64_t ntail = ceil_div(h->l - body_end, fast::SUB);  // residual-window items
+    const int64_t n_parts = nfull + ntail;                       // <= n_sub + 1
+    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB)) + 1;
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * H * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap * H);
@@ -616,7 +622,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     a.l = (int)h->l;
     a.kg = (int)h->kg();
     a.vg = (int)h->vg();
-    a.n_sub = (int)n_sub;
+    a.n_sub = (int)n_parts;
     a.q = q;
     a.qscale = qscale;
     a.part_o = h->part_o;
@@ -652,7 +658,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         KIVI_CUDA(dalloc(&h->work, 1));
     }
-    const bool has_tail = n_sub > nfull;
+    const bool has_tail = ntail > 0;
     static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
     cudaStream_t tail_st = nfull > 0 ? h->side : st;
     if (has_tail) {
@@ -662,9 +668,9 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
             KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
         }
         a.k_first = (int)nfull;
-        a.t_first = (int)(nfull * fast::SUB);
+        a.t_first = (int)body_end;
         a.sub = fast::SUB;
-        a.n_per_unit = (int)(n_sub - nfull);
+        a.n_per_unit = (int)ntail;
         a.n_items = (int)(U * a.n_per_unit);
         if (tail_st != st) {
             // one-warp CTAs (27 KB) so two tensor-core CTAs still fit beside one
@@ -683,6 +689,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         a.k_first = 0;
         a.t_first = 0;
         a.sub = fast::SUB;
+        a.body_end = (int)body_end;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
         a.work = h->work;
@@ -700,7 +707,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     }
     h->main_launches++;
     gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
-        h->part_o, h->part_ml, (int)n_sub, H, out, weights ? h->stats : nullptr,
+        h->part_o, h->part_ml, (int)n_parts, H, out, weights ? h->stats : nullptr,
         U * H < 4 * num_sms());
     KIVI_LAUNCHED();
     h->total_launches++;
