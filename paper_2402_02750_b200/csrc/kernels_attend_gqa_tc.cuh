@@ -69,7 +69,14 @@ using fast::SUB;
 #define KIVI_GQA_TC_WARPS 4
 #endif
 constexpr int WARPS = KIVI_GQA_TC_WARPS;   // warps per CTA
-constexpr int MIN_CTAS = KT == 2 ? 3 : 2;
+#ifndef KIVI_GQA_TC_MIN_CTAS
+#define KIVI_GQA_TC_MIN_CTAS (KT == 2 ? 3 : 2)
+#endif
+constexpr int MIN_CTAS = KIVI_GQA_TC_MIN_CTAS;
+#ifndef KIVI_GQA_KEY_SPLIT
+#define KIVI_GQA_KEY_SPLIT 1
+#endif
+constexpr int KEY_SPLIT = KIVI_GQA_KEY_SPLIT;  // 1: two accumulator chains per key tile
 constexpr int BFK_ROW = 9;        // uint2 per consumer lane in the key B buffer (8 K steps + pad)
 constexpr int BFV_CG = 72;        // 32-bit words per channel group in the value B buffer (64 + pad)
 constexpr int BIAS_ROW = 17;      // floats per lane row of the key-bias transpose
@@ -242,7 +249,11 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     // consumer: 8 K steps x 2 MMAs of tile T, then its logits
     auto consume = [&](int T) {
         const uint2* bfk = reinterpret_cast<const uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
-        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+        // even / odd K steps accumulate separately: two independent HMMA
+        // chains per token half
+        float4 acc[2][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[e][0] = acc[e][1] = make_float4(0.f, 0.f, 0.f, 0.f);
         const uint8_t* ct = slot + T * 1024 + 4 * (g >> 2);
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
@@ -255,7 +266,12 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
             const CodeQuad c23 = code_quad(__byte_perm(w2, w3, sel));
             uint2 b = make_uint2(0u, 0u);
             if (g < 2 * H) b = bfk[lane * BFK_ROW + s];
-            mma_f16_x2(acc0, acc1, c01, c23, b.x, b.y);
+            mma_f16_x2(acc[s & KEY_SPLIT][0], acc[s & KEY_SPLIT][1], c01, c23, b.x, b.y);
+        }
+        float4 acc0 = acc[0][0], acc1 = acc[0][1];
+        if (KEY_SPLIT) {
+            acc0.x += acc[1][0].x; acc0.y += acc[1][0].y; acc0.z += acc[1][0].z; acc0.w += acc[1][0].w;
+            acc1.x += acc[1][1].x; acc1.y += acc[1][1].y; acc1.z += acc[1][1].z; acc1.w += acc[1][1].w;
         }
         const float bias = __shfl_sync(FULL, bs, (T * H + t) & 15);  // column T*H+t
         if (t < H) {
