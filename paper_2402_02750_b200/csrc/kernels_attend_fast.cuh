@@ -773,7 +773,10 @@ __device__ __forceinline__ void issue_job(const FastArgs& a, int u, const JobDes
 // NW warps per CTA: 4 when the tail runs alone; 1 when it runs beside the
 // body kernel on a side stream, so its CTAs fit in the shared memory the
 // body CTAs leave free and every tail item gets its own warp.
-template <int B, int NW = WARPS>
+// APP: compile the fused-append and single-launch (gbar) modes in.  Their
+// append / quantize / merge code is ~20K SASS instructions; the default tail
+// kernel leaves it out to keep its instruction footprint small.
+template <int B, int NW = WARPS, bool APP = false>
 __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     using PB = P<B>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -797,7 +800,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     // Item order.  Default: item i to warp i mod tw.  Fused append: a warp owns
     // whole units (u = gw, gw + tw, ...) and walks each unit's items in order,
     // appending the unit's new token before issuing its first job.
-    const bool fused = a.l_app >= 0 && !a.gbar;
+    const bool fused = APP && a.l_app >= 0 && !a.gbar;
     const int nper = a.n_per_unit;
     const int n_units = a.n_items / nper;
     auto first_item = [&]() { return fused ? gw * nper : gw; };
@@ -806,14 +809,16 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
         return (it % nper == nper - 1) ? it + 1 + (tw - 1) * nper : it + 1;
     };
     auto enter_unit = [&](int it) {  // whole warp
-        if (fused && it < a.n_items && it % nper == 0) {
-            append_unit_fast<B>(a.c, a.tk, a.tv, a.l_app, it / nper, lane);
-            fence_proxy_async_global();  // the unit's TMA reads follow its append
-            __syncwarp();
+        if constexpr (APP) {
+            if (fused && it < a.n_items && it % nper == 0) {
+                append_unit_fast<B>(a.c, a.tk, a.tv, a.l_app, it / nper, lane);
+                fence_proxy_async_global();  // the unit's TMA reads follow its append
+                __syncwarp();
+            }
         }
     };
     (void)n_units;
-    if (a.gbar) {
+    if (APP && a.gbar) {
         // single-launch decode: appends, then a grid-wide barrier
         if (gw < n_units) {
             append_unit_fast<B>(a.c, a.tk, a.tv, a.l_app, gw, lane);
@@ -830,7 +835,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     }
     int f_item = first_item(), f_job = 0;
     ItemPlan f_plan{};
-    if (!a.gbar) enter_unit(f_item);
+    if (!(APP && a.gbar)) enter_unit(f_item);
     if (f_item < a.n_items) f_plan = plan_item<B>(a, f_item);
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
                 const int64_t pi = (int64_t)p.u * a.n_sub + p.k;
                 v_finalize<B>(slot, vacc, zacc0, zacc1, facc, ml, a.part_o + pi * D,
                               a.part_ml + pi, lane);
-                if (a.gbar) {
+                if (APP && a.gbar) {
                     // the unit's last partial merges the unit
                     __threadfence();
                     __syncwarp();

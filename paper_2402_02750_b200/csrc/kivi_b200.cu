@@ -364,10 +364,10 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
     const int smem = fast::WS2::STRIDE * fast::WARPS;
     static int per_sm = 0;
     if (!per_sm) {
-        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, fast::WARPS, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
+            &per_sm, fast::attend_tail_kernel<B, fast::WARPS, true>, fast::WARPS * 32, smem));
         if (per_sm < 1) per_sm = 1;
     }
     fast::FastArgs a{};
@@ -407,7 +407,7 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
         cudaEventRecord(e0, st);
     }
     void* args[] = {&a};
-    KIVI_CUDA(cudaLaunchCooperativeKernel((const void*)fast::attend_tail_kernel<B>, dim3((unsigned)grid),
+    KIVI_CUDA(cudaLaunchCooperativeKernel((const void*)fast::attend_tail_kernel<B, fast::WARPS, true>, dim3((unsigned)grid),
                                           dim3(fast::WARPS * 32), args, (size_t)smem, st));
     KIVI_LAUNCHED();
     if (h->profile) {
@@ -489,6 +489,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_body));
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, fast::WARPS, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, 1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        fast::WS2::STRIDE));
@@ -532,7 +534,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.tk = tk;
         a.tv = tv;
         a.l_app = (int)l_app;
-        if (nfull > 0 && tail_st != st && tail_warp_ctas) {
+        if (nfull > 0 && tail_st != st && tail_warp_ctas && l_app < 0) {
             // one-warp CTAs beside the body kernel: every tail item its own warp
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_warp_ctas,
                                                    a.n_items);
@@ -541,7 +543,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             const int per_sm = (nfull > 0 && tail_st != st) ? tail_ctas : h->fast_per_sm[B][1];
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
                                                    ceil_div(a.n_items, fast::WARPS));
-            fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
+            if (l_app >= 0)  // fused append: the variant carrying the append code
+                fast::attend_tail_kernel<B, fast::WARPS, true>
+                    <<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
+            else
+                fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
         }
         KIVI_LAUNCHED();
         if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
