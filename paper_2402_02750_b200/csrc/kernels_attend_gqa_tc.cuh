@@ -73,6 +73,9 @@ constexpr int WARPS = KIVI_GQA_TC_WARPS;   // warps per CTA
 #define KIVI_GQA_TC_MIN_CTAS (KT == 2 ? 3 : 2)
 #endif
 constexpr int MIN_CTAS = KIVI_GQA_TC_MIN_CTAS;
+#ifndef KIVI_GQA_UNROLL
+#define KIVI_GQA_UNROLL 1
+#endif
 #ifndef KIVI_GQA_KEY_SPLIT
 #define KIVI_GQA_KEY_SPLIT 1
 #endif
@@ -288,12 +291,23 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     // consumer (tile T+1's producer writes the buffer tile T-1 read before
     // the barrier of tile T).  Building tile T+1 during tile T's MMAs measured
     // slower (374 vs 360 us on C3): register pressure, no extra overlap.
+#if KIVI_GQA_UNROLL
+#pragma unroll
+    for (int T = 0; T < KT; ++T) {
+        if (T < ntl) {
+            produce(T);
+            __syncwarp();
+            consume(T);
+        }
+    }
+#else
 #pragma unroll 1
     for (int T = 0; T < ntl; ++T) {
         produce(T);
         __syncwarp();
         consume(T);
     }
+#endif
     __syncwarp();  // the next job's producer overwrites the buffers
 }
 
@@ -369,17 +383,18 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
 // (this lane's share of sum_t p_h[t] z[t][cg = lane & 3], token pair halves).  eb_run is the running
 // exponent byte (the larger of all jobs so far: smaller 2^E).
 // -------------------------------------------------------------------------
-template <int H>
+template <int H, bool FULL = true>
 __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_src, float4 (&vacc)[4][2],
                                           float2 (&zs)[H], int& eb_run, bool first, uint8_t* bf,
                                           int lane, uint32_t sel, int ntok = VT) {
+    if constexpr (FULL) ntok = VT;
     const int g = lane >> 2, t = lane & 3;
     const float4* pairs4 = reinterpret_cast<const float4*>(slot + VT * 32);
     const float2* pairs2 = reinterpret_cast<const float2*>(slot + VT * 32);
     float dmax = 0.f;
 #pragma unroll
     for (int i = 0; i < VT / 16; ++i) {
-        if ((lane + 32 * i) / 2 < ntok) {  // float4 f holds token f / 2
+        if (FULL || (lane + 32 * i) / 2 < ntok) {  // float4 f holds token f / 2
             const float4 pr = pairs4[lane + 32 * i];
             dmax = fmaxf(dmax, fmaxf(pr.y - pr.x, pr.w - pr.z));
         }
@@ -408,8 +423,8 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
         const int ta = 16 * s + toff, tb = ta + 4;
         // tokens past a partial item's end: zero operands (their slot bytes
         // were not loaded)
-        const float2 pa = ta < ntok ? pairs2[ta * 4 + cgp] : make_float2(0.f, 0.f);
-        const float2 pb = tb < ntok ? pairs2[tb * 4 + cgp] : make_float2(0.f, 0.f);
+        const float2 pa = (FULL || ta < ntok) ? pairs2[ta * 4 + cgp] : make_float2(0.f, 0.f);
+        const float2 pb = (FULL || tb < ntok) ? pairs2[tb * 4 + cgp] : make_float2(0.f, 0.f);
         const float2 d2 = __fmul2_rn(make_float2(pa.y - pa.x, pb.y - pb.x), make_float2(f, f));
         const float2 z2 = make_float2(pa.x, pb.x);
         float2 P[H];  // (p_h[ta], p_h[tb])
@@ -451,6 +466,17 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
         }
     };
     // one warp barrier per K step (two buffers, as in key_job)
+#if KIVI_GQA_UNROLL
+    if constexpr (FULL) {
+#pragma unroll
+        for (int s = 0; s < VT / 16; ++s) {
+            produce(s);
+            __syncwarp();
+            consume(s);
+        }
+        return;
+    }
+#endif
 #pragma unroll 1
     for (int s = 0; s < (ntok + 15) / 16; ++s) {
         produce(s);
@@ -651,9 +677,12 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
         for (int jv = 0; jv < NVJ; ++jv) {
             uint8_t* slot = wait_slot();
             const int ntok = min(VT, max(0, Ti - jv * VT));
-            if (ntok)
-                value_job<H>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane, sel,
-                             ntok);
+            if (ntok == VT)
+                value_job<H, true>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
+                                   sel);
+            else if (ntok)
+                value_job<H, false>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
+                                    sel, ntok);
             if (jv == NVJ - 1) {
                 const int64_t pi = ((int64_t)u * a.n_sub + k) * H;
                 value_finalize<H>(vacc, zs, eb_run, ml, zsm, a.part_o + pi * D, a.part_ml + pi, lane);
