@@ -144,6 +144,7 @@ struct FastArgs {
     float2* part_ml;    // [units][n_sub]   (max, sum) in log2 domain
     float* wlog;        // [units][l] log2-domain logits, or null
     int* work;          // body kernel: dynamic item counter (zeroed before launch)
+    int prefetch;       // tail kernel: L2-prefetch each item's fp32 rows
     int body_end;       // tensor-core GQA body: tokens it covers (multiple of 32;
                         // its last item per unit may be partial)
     // fused append (tail kernel only): when l_app >= 0 the tail kernel first
@@ -833,6 +834,26 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
         __syncwarp();
         fence_proxy_async_global();  // this warp's TMA reads follow every append
     }
+    // The item's fp32 residual rows (up to 2 x 64 KB) are a chain of 16-row
+    // jobs through two slots; with a.prefetch they are all prefetched into L2
+    // when the item's first job is issued, turning the chain's HBM round trips
+    // into L2 hits.  Used on the few-unit route (C1: 22.2 -> 21.2 us); beside
+    // the body kernel it costs more than it saves (C2 248 -> 258 us).
+    auto prefetch_rows = [&](const ItemPlan& p) {
+        const CacheDev& c = a.c;
+        const int kf0 = max(p.t0, a.kg);
+        if (p.t1 > kf0)
+            bulk_prefetch_l2(c.kring + p.u * c.ring_ustride + (int64_t)(kf0 - a.kg) * D,
+                             (uint32_t)(p.t1 - kf0) * D * 4);
+        const int vf0 = max(p.t0, a.vg);
+        if (p.t1 > vf0) {
+            const float* ring = c.vring + p.u * c.ring_ustride;
+            const int r0 = vf0 % c.R, n = p.t1 - vf0;
+            const int n1 = min(n, c.R - r0);
+            bulk_prefetch_l2(ring + (int64_t)r0 * D, (uint32_t)n1 * D * 4);
+            if (n > n1) bulk_prefetch_l2(ring, (uint32_t)(n - n1) * D * 4);
+        }
+    };
     int f_item = first_item(), f_job = 0;
     ItemPlan f_plan{};
     if (!(APP && a.gbar)) enter_unit(f_item);
@@ -840,6 +861,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
+            if (a.prefetch && f_job == 0) prefetch_rows(f_plan);
             const JobDesc jd = job_of<B>(a, f_plan, f_job);
             fence_proxy_async_smem();
             issue_job<B>(a, f_plan.u, jd, f_job == 0, wbase + s * SLOT, qraw, &bars[s], policy);

@@ -534,6 +534,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.tk = tk;
         a.tv = tv;
         a.l_app = (int)l_app;
+        a.prefetch = latency_bound ? 1 : 0;
         if (nfull > 0 && tail_st != st && tail_warp_ctas && l_app < 0) {
             // one-warp CTAs beside the body kernel: every tail item its own warp
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_warp_ctas,
