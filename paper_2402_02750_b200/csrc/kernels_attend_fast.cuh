@@ -58,6 +58,9 @@ constexpr int KQ_UNROLL = KIVI_KQ_UNROLL;
 
 // w >> K on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF): the body
 // kernel is ALU-bound on the code extraction, the FMA pipe has headroom.
+#ifndef KIVI_VQ_UNROLL
+#define KIVI_VQ_UNROLL 1
+#endif
 #ifndef KIVI_SHR_FMA
 #define KIVI_SHR_FMA 1
 #endif
@@ -396,13 +399,37 @@ __device__ __forceinline__ float2 softmax_item(float* probs, int ntok, float* wl
 
 // Quantized value tokens -> P.V accumulators.  Lane = (jj, h): token offset
 // jj in 0..15, channel half h (channels 64h .. 64h+63 = groups 2h, 2h+1).
-template <int B>
+// NT > 0: n == NT, a multiple of 16 (body jobs): the token loop is unrolled,
+// with no trip-count test or prefetch register rotation.
+template <int B, int NT = 0>
 __device__ __forceinline__ void vq_tokens_accumulate(const uint8_t* slot, const float* pr_tok, int n,
                                                      float ksc, float2* vacc, float& zacc0,
                                                      float& zacc1, int lane) {
     using PB = P<B>;
     const int h = lane & 1, jj = lane >> 1;
     const uint8_t* pairs = slot + PB::VQ_TOK * PB::TOK_CODE;
+#if KIVI_VQ_UNROLL
+    if constexpr (B == 2 && NT > 0) {
+        static_assert(NT % 16 == 0, "unrolled value job: whole 16-token rounds");
+#pragma unroll
+        for (int i = 0; i < NT / 16; ++i) {
+            const int t = jj + 16 * i;
+            const uint4 cw = *reinterpret_cast<const uint4*>(slot + t * PB::TOK_CODE + h * 16);
+            const float4 pr = *reinterpret_cast<const float4*>(pairs + t * 32 + h * 16);
+            const float pt = pr_tok[t];
+            const float pk = pt * ksc;
+            const float ws0 = pk * (pr.y - pr.x);
+            const float ws1 = pk * (pr.w - pr.z);
+            zacc0 = fmaf(pt, pr.x, zacc0);
+            zacc1 = fmaf(pt, pr.z, zacc1);
+            PB::fma_word(vacc, cw.x, ws0);
+            PB::fma_word(vacc + 8, cw.y, ws0);
+            PB::fma_word(vacc + 16, cw.z, ws1);
+            PB::fma_word(vacc + 24, cw.w, ws1);
+        }
+        return;
+    }
+#endif
     if constexpr (B == 2) {
         int t = jj;
         uint4 cw = make_uint4(0, 0, 0, 0);
@@ -557,8 +584,6 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     __syncwarp();
     const uint64_t policy = make_evict_first_policy();
     const CacheDev& c = a.c;
-    const int gw = blockIdx.x * WARPS + warp;
-    const int tw = gridDim.x * WARPS;
     const int nper = a.n_per_unit;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
 
@@ -646,8 +671,8 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
 #pragma unroll 1
         for (int jv = 0; jv < NVJ; ++jv) {
             uint8_t* slot = wait_slot();
-            vq_tokens_accumulate<B>(slot, probs + jv * PB::VQ_TOK, PB::VQ_TOK, ksc, vacc, zacc0,
-                                    zacc1, lane);
+            vq_tokens_accumulate<B, PB::VQ_TOK>(slot, probs + jv * PB::VQ_TOK, PB::VQ_TOK, ksc,
+                                                vacc, zacc0, zacc1, lane);
             if (jv == NVJ - 1) {
                 const int64_t pi = (int64_t)u * a.n_sub + k;
                 v_finalize<B>(slot, vacc, zacc0, zacc1, make_float4(0.f, 0.f, 0.f, 0.f), ml,
