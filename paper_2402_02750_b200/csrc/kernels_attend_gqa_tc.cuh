@@ -474,14 +474,15 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
             __syncwarp();
             consume(s);
         }
-        return;
-    }
+    } else
 #endif
+    {
 #pragma unroll 1
-    for (int s = 0; s < (ntok + 15) / 16; ++s) {
-        produce(s);
-        __syncwarp();
-        consume(s);
+        for (int s = 0; s < (ntok + 15) / 16; ++s) {
+            produce(s);
+            __syncwarp();
+            consume(s);
+        }
     }
 }
 
