@@ -222,11 +222,14 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
  * supported, else generic), 1 = force generic, 2 = force fast (error if the
  * shape is unsupported). */
 kivi_status kivi_set_attend_path(kivi_cache* cache, int32_t path);
-/* When enabled, kivi_attend records CUDA events around its main kernel. */
+/* enable = 0: off.  enable = k >= 1: kivi_attend / kivi_decode record CUDA
+ * events around the main attend kernel of every k-th call (k > 1 keeps the
+ * host cost of the events off latency-bound steps). */
 kivi_status kivi_profile_enable(kivi_cache* cache, int32_t enable);
 /* Synchronises the recorded events and returns the summed main-kernel time,
- * the number of main-kernel launches and the total number of kernels this
- * library launched for the cache since the last reset; then resets. */
+ * the number of main-kernel launches timed (summed into main_kernel_ms) and
+ * the total number of kernels this library launched for the cache since the
+ * last reset; then resets. */
 kivi_status kivi_profile_read(kivi_cache* cache, double* main_kernel_ms, int64_t* main_launches,
                               int64_t* total_launches);
 /* Algorithmic HBM bytes the attend kernel must read + write per unit for the

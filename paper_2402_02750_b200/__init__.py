@@ -374,8 +374,13 @@ class KVCache:
         return k, v
 
     # ---- measurement hooks ---------------------------------------------------
-    def profile_enable(self, on: bool = True) -> None:
-        _check(lib().kivi_profile_enable(self._h, int(bool(on))))
+    def profile_enable(self, on=True) -> None:
+        """on: False/0 = off; True/1 = time every attend launch; k > 1 = time
+        every k-th launch (include/kivi_b200.h kivi_profile_enable)."""
+        k = int(on) if not isinstance(on, bool) else int(on)
+        if k < 0:
+            raise UsageError("profile stride must be >= 0")
+        _check(lib().kivi_profile_enable(self._h, k))
 
     def profile_read(self):
         ms = ctypes.c_double()

@@ -141,6 +141,9 @@ struct kivi_cache {
 
     // profiling
     bool profile = false;
+    int profile_stride = 1;     // time every profile_stride-th attend launch
+    int64_t profile_seq = 0;    // attend launches seen while profiling
+    bool prof_now = false;      // the current attend launch is timed
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
     int64_t main_launches = 0;
     int64_t total_launches = 0;
@@ -401,7 +404,8 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
     a.out = out;
     a.stats = weights ? h->stats : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->profile) {
+    h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
+    if (h->prof_now) {
         e0 = h->take_event();
         e1 = h->take_event();
         cudaEventRecord(e0, st);
@@ -410,11 +414,11 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
     KIVI_CUDA(cudaLaunchCooperativeKernel((const void*)fast::attend_tail_kernel<B, fast::WARPS, true>, dim3((unsigned)grid),
                                           dim3(fast::WARPS * 32), args, (size_t)smem, st));
     KIVI_LAUNCHED();
-    if (h->profile) {
+    if (h->prof_now) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
+        h->main_launches++;
     }
-    h->main_launches++;
     h->total_launches++;
     if (weights) {
         fast::normalize_weights_kernel<<<grid_for(U * h->l), 256, 0, st>>>(weights, h->stats, h->l,
@@ -503,7 +507,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         h->fast_per_sm[B][1] = per_sm < 1 ? 1 : per_sm;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->profile) {
+    h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
+    if (h->prof_now) {
         e0 = h->take_event();
         e1 = h->take_event();
         cudaEventRecord(e0, st);
@@ -578,11 +583,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         h->total_launches++;
     }
     if (has_tail && tail_st != st) KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (h->profile) {
+    if (h->prof_now) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
+        h->main_launches++;
     }
-    h->main_launches++;
     // K5: merge the per-item partials (a separate launch keeps the merge work
     // balanced; fusing it into the attend tail serialised it on the last warps)
     fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
@@ -654,7 +659,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         h->fast_per_sm[key][3] = per_sm < 1 ? 1 : per_sm;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->profile) {
+    h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
+    if (h->prof_now) {
         e0 = h->take_event();
         e1 = h->take_event();
         cudaEventRecord(e0, st);
@@ -708,11 +714,11 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         h->total_launches++;
     }
     if (has_tail && tail_st != st) KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (h->profile) {
+    if (h->prof_now) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
+        h->main_launches++;
     }
-    h->main_launches++;
     gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
         h->part_o, h->part_ml, (int)n_parts, H, out, weights ? h->stats : nullptr,
         U * H < 4 * num_sms());
@@ -746,18 +752,19 @@ kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, f
     a.scale_logits = scale_logits;
     const size_t smem = sizeof(float) * (size_t)(h->cfg.head_dim + 32);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->profile) {
+    h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
+    if (h->prof_now) {
         e0 = h->take_event();
         e1 = h->take_event();
         cudaEventRecord(e0, st);
     }
     attend_generic_kernel<<<(unsigned)rows, 256, smem, st>>>(a);
     KIVI_LAUNCHED();
-    if (h->profile) {
+    if (h->prof_now) {
         cudaEventRecord(e1, st);
         h->events.emplace_back(e0, e1);
+        h->main_launches++;
     }
-    h->main_launches++;
     h->total_launches++;
     return KIVI_OK;
 }
@@ -1485,7 +1492,10 @@ kivi_status kivi_set_attend_path(kivi_cache* h, int32_t path) {
 
 kivi_status kivi_profile_enable(kivi_cache* h, int32_t enable) {
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
+    if (enable < 0) return fail(KIVI_ERR_USAGE, "profile stride must be >= 0");
     h->profile = enable != 0;
+    h->profile_stride = enable > 1 ? enable : 1;
+    h->profile_seq = 0;
     return KIVI_OK;
 }
 

@@ -264,6 +264,31 @@ def test_fast_equals_generic_closely(cuda):
         assert rel_l2(oa[u], ob[u]) <= 1e-5
 
 
+def test_profile_stride_times_every_kth_attend(cuda):
+    """kivi_profile_enable(k): events around every k-th attend launch only
+    (bench.py samples so the events' host cost stays off latency-bound steps)."""
+    rng = np.random.default_rng(5)
+    U, d, l0 = 4, 128, 300
+    K = rnd(rng, U, l0, d)
+    c = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    c.prefill(dev(K), dev(K))
+    q = dev(rnd(rng, U, 1, d))
+    c.profile_enable(3)
+    for _ in range(7):
+        c.attend(q)
+    ms, n, tot = c.profile_read()
+    assert n == 3 and ms > 0 and tot >= 7  # launches 0, 3, 6 timed
+    c.profile_enable(1)
+    c.attend(q)
+    c.attend(q)
+    assert c.profile_read()[1] == 2
+    c.profile_enable(False)
+    c.attend(q)
+    assert c.profile_read()[1] == 0
+    with pytest.raises(kb.UsageError):
+        c.profile_enable(-1)
+
+
 def run_gqa(cfg, U, qpk, l0, steps, path, seed, weights=False, kscale=1.0, vscale=1.0,
             qscale=1.0, outliers=()):
     """GQA: one append per unit, q_per_kv query heads; the reference emulates
