@@ -197,6 +197,14 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
         : "memory");
 }
 
+// Programmatic dependent launch.  A kernel launched with the
+// programmatic-serialization attribute may start before its predecessor in
+// the stream has finished; it must pdl_wait() before touching memory the
+// predecessor writes (a no-op for a normal launch).  pdl_trigger() lets the
+// dependent's CTAs be scheduled once every CTA of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // Bulk prefetch of [src, src + bytes) into L2 (no shared memory, no
 // completion tracking); bytes a multiple of 16, src 16-byte aligned.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

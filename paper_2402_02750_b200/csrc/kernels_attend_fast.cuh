@@ -805,6 +805,8 @@ __device__ __forceinline__ void issue_job(const FastArgs& a, int u, const JobDes
 template <int B, int NW = WARPS, bool APP = false>
 __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     using PB = P<B>;
+    pdl_wait();     // the append before it (programmatic launch, few-unit route)
+    pdl_trigger();  // ... and the combine after it
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* wbase = smem_raw + warp * WS2::STRIDE;
@@ -1037,6 +1039,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ 
                                                       const float2* __restrict__ part_ml, int n_sub,
                                                       float* __restrict__ out,
                                                       float2* __restrict__ stats, int parallel) {
+    pdl_wait();
     const int64_t u = blockIdx.x;
     if (parallel)
         combine_row(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D, stats ? stats + u : nullptr);

@@ -257,6 +257,7 @@ __device__ __forceinline__ void append_unit_fast(const CacheDev& c, const float*
 template <int B>
 __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const float* __restrict__ tk,
                                                           const float* __restrict__ tv, int64_t l) {
+    pdl_trigger();  // the attend launch may be scheduled behind this one
     const int lane = threadIdx.x & 31;
     const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (u >= c.n_units) return;

@@ -429,6 +429,24 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
     return KIVI_OK;
 }
 
+// Launch with programmatic stream serialization (kernel must pdl_wait()
+// before reading what the previous kernel in the stream writes).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st, const float* tk = nullptr, const float* tv = nullptr,
@@ -520,6 +538,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         KIVI_CUDA(dalloc(&h->work, 1));
     }
     const bool has_tail = n_sub > nfull;
+    static const int use_pdl = env_int("KIVI_PDL", 1);
     static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
     static const int tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
     static const int tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
@@ -552,6 +571,10 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             if (l_app >= 0)  // fused append: the variant carrying the append code
                 fast::attend_tail_kernel<B, fast::WARPS, true>
                     <<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
+            else if (use_pdl && tail_st == st && !h->prof_now)
+                // few-unit route: the latency chain append -> attend -> combine
+                KIVI_CUDA(launch_pdl(fast::attend_tail_kernel<B>, dim3((unsigned)grid),
+                                     dim3(fast::WARPS * 32), (size_t)smem, st, a));
             else
                 fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
         }
@@ -590,9 +613,14 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     }
     // K5: merge the per-item partials (a separate launch keeps the merge work
     // balanced; fusing it into the attend tail serialised it on the last warps)
-    fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
-                                                          weights ? h->stats : nullptr,
-                                                          U < 4 * num_sms());
+    if (use_pdl && nfull == 0 && !h->prof_now)
+        KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)U), dim3(fast::D), 0, st,
+                             (const float*)h->part_o, (const float2*)h->part_ml, (int)n_sub, out,
+                             weights ? h->stats : (float2*)nullptr, (int)(U < 4 * num_sms())));
+    else
+        fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub,
+                                                              out, weights ? h->stats : nullptr,
+                                                              U < 4 * num_sms());
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
