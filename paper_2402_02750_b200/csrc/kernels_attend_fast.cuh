@@ -146,7 +146,8 @@ struct FastArgs {
     float* part_o;      // [units][n_sub][128]
     float2* part_ml;    // [units][n_sub]   (max, sum) in log2 domain
     float* wlog;        // [units][l] log2-domain logits, or null
-    int* work;          // body kernel: dynamic item counter (zeroed before launch)
+    int* work;          // body kernel: dynamic item counter (zero at launch)
+    int* work_clear;    // body kernel: a later launch's counter, zeroed here
     int prefetch;       // tail kernel: L2-prefetch each item's fp32 rows
     int body_end;       // tensor-core GQA body: tokens it covers (multiple of 32;
                         // its last item per unit may be partial)
@@ -586,6 +587,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     const CacheDev& c = a.c;
     const int nper = a.n_per_unit;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.work_clear) *a.work_clear = 0;
 
     // Items are taken dynamically (atomic counter), one item ahead of use, so
     // CTAs that start late — e.g. after a concurrently running tail kernel
@@ -681,6 +683,10 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             release_slot();
         }
     }
+    // programmatic launch after the residual-window kernel (one stream): let
+    // the combine be scheduled, and finish only once that kernel has finished
+    pdl_trigger();
+    pdl_wait();
 }
 
 // ===================== K4b: tail kernel (items with residual tokens) ========

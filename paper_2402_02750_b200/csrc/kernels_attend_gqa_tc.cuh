@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     const CacheDev& c = a.c;
     const int nper = a.n_per_unit;
     const uint32_t sel = (uint32_t)(lane >> 2 & 3) * 0x1111u + 0x4400u;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.work_clear) *a.work_clear = 0;
 
     auto grab = [&]() -> int {
         int v = 0;

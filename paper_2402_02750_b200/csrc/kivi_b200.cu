@@ -129,7 +129,8 @@ struct kivi_cache {
     // fast attend: the tail kernel runs on a side stream next to the body kernel
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    int* work = nullptr;  // body kernel dynamic item counter
+    int* work = nullptr;  // body kernels' dynamic item counters: a ring of WORK_SLOTS
+    int64_t work_seq = 0; // body launches so far (slot = work_seq % WORK_SLOTS)
     cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
     cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
     unsigned long long* small_sync = nullptr;  // [1 + n_units] single-launch decode counters
@@ -429,6 +430,17 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
     return KIVI_OK;
 }
 
+// Body kernels take items from a counter: launch i uses slot i % WORK_SLOTS
+// and zeroes slot (i + WORK_SLOTS/2) % WORK_SLOTS for a later launch (that
+// slot's last user finished WORK_SLOTS/2 launches ago), so no memset sits
+// between the kernels of a decode step.
+constexpr int WORK_SLOTS = 64;
+static void take_work_slot(kivi_cache* h, fast::FastArgs& a) {
+    const int s = (int)(h->work_seq++ % WORK_SLOTS);
+    a.work = h->work + s;
+    a.work_clear = h->work + (s + WORK_SLOTS / 2) % WORK_SLOTS;
+}
+
 // Launch with programmatic stream serialization (kernel must pdl_wait()
 // before reading what the previous kernel in the stream writes).
 template <typename... KArgs, typename... Args>
@@ -535,17 +547,26 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         KIVI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-        KIVI_CUDA(dalloc(&h->work, 1));
+        KIVI_CUDA(dalloc(&h->work, WORK_SLOTS));
+        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int) * WORK_SLOTS, st));
     }
     const bool has_tail = n_sub > nfull;
     static const int use_pdl = env_int("KIVI_PDL", 1);
     static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
     static const int tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
     static const int tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
-    cudaStream_t tail_st = (tail_side && nfull > 0) ? h->side : st;
+    // Body and tail concurrently.  Default: one stream, programmatic launches
+    // (append -> tail -> body -> combine): the tail waits for the append, then
+    // triggers, so the body's CTAs start beside it (the body reads only what
+    // the append wrote, complete once the tail runs) and wait for the tail
+    // only at their end, before the combine.  KIVI_PDL=0: tail on a side
+    // stream with fork / join events.
+    const bool one_stream = use_pdl && nfull > 0 && has_tail && l_app < 0 && !tail_warp_ctas &&
+                            !(B == 2 && mha_tc);
+    cudaStream_t tail_st = (tail_side && nfull > 0 && !one_stream) ? h->side : st;
     if (has_tail) {
-        // Tail items (residual fp32 tokens, latency-bound) on a side stream
-        // with one CTA per SM, concurrently with the ALU-bound body kernel.
+        // Tail items (residual fp32 tokens, latency-bound) with 2 CTAs per SM,
+        // concurrently with the ALU-bound body kernel.
         if (tail_st != st) {
             KIVI_CUDA(cudaEventRecord(h->ev_fork, st));
             KIVI_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
@@ -571,8 +592,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             if (l_app >= 0)  // fused append: the variant carrying the append code
                 fast::attend_tail_kernel<B, fast::WARPS, true>
                     <<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
-            else if (use_pdl && tail_st == st && !h->prof_now)
-                // few-unit route: the latency chain append -> attend -> combine
+            else if (use_pdl && tail_st == st && !(h->prof_now && !one_stream))
+                // few-unit route (append -> attend -> combine) or one_stream
                 KIVI_CUDA(launch_pdl(fast::attend_tail_kernel<B>, dim3((unsigned)grid),
                                      dim3(fast::WARPS * 32), (size_t)smem, st, a));
             else
@@ -589,8 +610,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.sub = fast::BSUB;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
-        a.work = h->work;
-        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int), st));
+        take_work_slot(h, a);
         if (B == 2 && mha_tc && fast::BSUB == fast::SUB) {
             // tensor-core body (kernels_attend_gqa_tc.cuh with one query head)
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][2],
@@ -600,7 +620,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         } else {
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
                                                    ceil_div(a.n_items, fast::WARPS));
-            fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
+            if (one_stream)
+                KIVI_CUDA(launch_pdl(fast::attend_body_kernel<B>, dim3((unsigned)grid),
+                                     dim3(fast::WARPS * 32), (size_t)smem_body, st, a));
+            else
+                fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
         }
         KIVI_LAUNCHED();
         h->total_launches++;
@@ -613,7 +637,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     }
     // K5: merge the per-item partials (a separate launch keeps the merge work
     // balanced; fusing it into the attend tail serialised it on the last warps)
-    if (use_pdl && nfull == 0 && !h->prof_now)
+    if (use_pdl && ((nfull == 0 && !h->prof_now) || (one_stream && !h->prof_now)))
         KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)U), dim3(fast::D), 0, st,
                              (const float*)h->part_o, (const float2*)h->part_ml, (int)n_sub, out,
                              weights ? h->stats : (float2*)nullptr, (int)(U < 4 * num_sms())));
@@ -697,7 +721,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         KIVI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-        KIVI_CUDA(dalloc(&h->work, 1));
+        KIVI_CUDA(dalloc(&h->work, WORK_SLOTS));
+        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int) * WORK_SLOTS, st));
     }
     const bool has_tail = ntail > 0;
     static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
@@ -733,8 +758,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         a.body_end = (int)body_end;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
-        a.work = h->work;
-        KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int), st));
+        take_work_slot(h, a);
         const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][3],
                                                ceil_div(a.n_items, gqa_tc::WARPS));
         gqa_tc::attend_gqa_tc_kernel<H><<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
