@@ -586,7 +586,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                                                    a.n_items);
             fast::attend_tail_kernel<B, 1><<<(unsigned)grid, 32, fast::WS2::STRIDE, tail_st>>>(a);
         } else {
-            const int per_sm = (nfull > 0 && tail_st != st) ? tail_ctas : h->fast_per_sm[B][1];
+            const int per_sm =
+                (nfull > 0 && (tail_st != st || one_stream)) ? tail_ctas : h->fast_per_sm[B][1];
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm,
                                                    ceil_div(a.n_items, fast::WARPS));
             if (l_app >= 0)  // fused append: the variant carrying the append code
