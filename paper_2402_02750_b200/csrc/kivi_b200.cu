@@ -441,6 +441,17 @@ static void take_work_slot(kivi_cache* h, fast::FastArgs& a) {
     a.work_clear = h->work + (s + WORK_SLOTS / 2) % WORK_SLOTS;
 }
 
+// K5 variant: the parallel-over-partials merge (weights computed once per
+// partial, then independent loads) measured faster at every config with the
+// partials L2-resident after the attend (C1 7.4 vs 12.8 us, C2 8.9 vs 10.0,
+// C3 17.7 vs 21.8, C5 13.2 vs 20.7 us per layer); KIVI_COMBINE_PARALLEL=0
+// selects the serial per-channel merge.
+static int combine_parallel(int64_t rows) {
+    static const int force = env_int("KIVI_COMBINE_PARALLEL", 1);
+    (void)rows;
+    return force ? 1 : 0;
+}
+
 // Launch with programmatic stream serialization (kernel must pdl_wait()
 // before reading what the previous kernel in the stream writes).
 template <typename... KArgs, typename... Args>
@@ -641,11 +652,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     if (use_pdl && ((nfull == 0 && !h->prof_now) || (one_stream && !h->prof_now)))
         KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)U), dim3(fast::D), 0, st,
                              (const float*)h->part_o, (const float2*)h->part_ml, (int)n_sub, out,
-                             weights ? h->stats : (float2*)nullptr, (int)(U < 4 * num_sms())));
+                             weights ? h->stats : (float2*)nullptr, combine_parallel(U)));
     else
         fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub,
                                                               out, weights ? h->stats : nullptr,
-                                                              U < 4 * num_sms());
+                                                              combine_parallel(U));
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
@@ -774,7 +785,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     }
     gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
         h->part_o, h->part_ml, (int)n_parts, H, out, weights ? h->stats : nullptr,
-        U * H < 4 * num_sms());
+        combine_parallel(U * H));
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
