@@ -158,7 +158,8 @@ def attend_kernel_name(qpk, units, ctx, sms=148):
                 "gqa::attend_gqa_kernel (residual items, side stream)")
     if units * -(-ctx // 256) < 4 * sms:
         return "kivi_b200::fast::attend_tail_kernel (few-unit route, 64-token items)"
-    return "kivi_b200::fast::attend_body_kernel + attend_tail_kernel (side stream)"
+    return ("kivi_b200::fast::attend_body_kernel + attend_tail_kernel (concurrent, one stream, "
+            "programmatic launch)")
 
 
 def dist_setup():
