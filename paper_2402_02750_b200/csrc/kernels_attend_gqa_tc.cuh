@@ -443,7 +443,10 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
         for (int h = 0; h < H; ++h) {
             uint32_t whi, wlo;
             split_pair(__fmul2_rn(P[h], d2), whi, wlo);
-            zs[h] = __ffma2_rn(P[h], z2, zs[h]);
+            // scalar FMAs: z2 = (pa.x, pb.x) is not a register pair, and
+            // FFMA2 on it cost ~6 register moves per step
+            zs[h].x = fmaf(P[h].x, z2.x, zs[h].x);
+            zs[h].y = fmaf(P[h].y, z2.y, zs[h].y);
             bv[cgp * BFV_CG + 2 * ((2 * h) * 4 + tcons) + which] = whi;
             bv[cgp * BFV_CG + 2 * ((2 * h + 1) * 4 + tcons) + which] = wlo;
         }
