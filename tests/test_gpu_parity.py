@@ -233,6 +233,45 @@ def test_decode_fast_vs_reference(cuda, bits, l0, route, monkeypatch):
     assert e_w <= 1e-5, e_w
 
 
+@pytest.mark.parametrize("small", ["0", "1"])
+@pytest.mark.parametrize("qpk", [1, 4])
+def test_layers_interleaved_on_one_stream(cuda, small, qpk, monkeypatch):
+    """A decode step over several layers: the caches' decodes are enqueued back to
+    back on one stream with no host sync (the programmatic launches of one layer
+    follow the previous layer's combine), each layer checked against its own
+    reference units."""
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", small)
+    ck = checker()
+    rng = np.random.default_rng(41 + qpk)
+    bits, G, R, d = 2, 32, 128, 128
+    U, L, l0, steps = 3, 3, 700, 3
+    caches, refs = [], []
+    for _ in range(L):
+        K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+        c = kb.KVCache(kb.CacheConfig(bits, G, R, d), U)
+        c.set_attend_path("fast")
+        c.prefill(dev(K), dev(V))
+        caches.append(c)
+        rs = [ck.unit(bits, G, R, d) for _ in range(U * qpk)]
+        for u in range(U):
+            for h in range(qpk):
+                rs[u * qpk + h].prefill(K[u], V[u])
+        refs.append(rs)
+    worst = 0.0
+    for _ in range(steps):
+        ins = [(rnd(rng, U, qpk, d), rnd(rng, U, d), rnd(rng, U, d)) for _ in range(L)]
+        outs = [c.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk)
+                for c, (q, tk, tv) in zip(caches, ins)]
+        for li in range(L):
+            q, tk, tv = ins[li]
+            o = outs[li].cpu().numpy()
+            for u in range(U):
+                for h in range(qpk):
+                    ro = refs[li][u * qpk + h].decode(q[u, h], tk[u], tv[u], scale_logits=True)
+                    worst = max(worst, rel_l2(o[u, h], ro))
+    assert worst <= 5e-5 if qpk > 1 else worst <= 1e-5, worst
+
+
 @pytest.mark.parametrize("route", [("0", "1", "0"), ("0", "0", "0"), ("1", "0", "0"),
                                    ("1", "0", "1")])
 @pytest.mark.parametrize("bits", [2, 4])
