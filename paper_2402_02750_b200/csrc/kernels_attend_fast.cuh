@@ -149,6 +149,12 @@ struct FastArgs {
     int* work;          // body kernel: dynamic item counter (zero at launch)
     int* work_clear;    // body kernel: a later launch's counter, zeroed here
     int prefetch;       // tail kernel: L2-prefetch each item's fp32 rows
+    // tail kernel, two item sizes per unit (few-unit route): items
+    // [0, n_a) are `sub` tokens from t_first up to t_b, items [n_a, n_per_unit)
+    // are sub_b tokens from t_b (the residual window's fp32 rows in short
+    // items, so no item is a long chain of dependent row jobs).  sub_b = 0:
+    // uniform items.
+    int sub_b, n_a, t_b;
     int body_end;       // tensor-core GQA body: tokens it covers (multiple of 32;
                         // its last item per unit may be partial)
     // fused append (tail kernel only): when l_app >= 0 the tail kernel first
@@ -702,9 +708,15 @@ template <int B>
 __device__ __forceinline__ ItemPlan plan_item(const FastArgs& a, int item) {
     ItemPlan p;
     p.u = item / a.n_per_unit;
-    p.k = a.k_first + (item - p.u * a.n_per_unit);
-    p.t0 = a.t_first + (p.k - a.k_first) * a.sub;
-    p.t1 = min(p.t0 + a.sub, a.l);
+    const int j = item - p.u * a.n_per_unit;
+    p.k = a.k_first + j;
+    if (a.sub_b > 0 && j >= a.n_a) {
+        p.t0 = a.t_b + (j - a.n_a) * a.sub_b;
+        p.t1 = min(p.t0 + a.sub_b, a.l);
+    } else {
+        p.t0 = a.t_first + j * a.sub;
+        p.t1 = min(p.t0 + a.sub, a.sub_b > 0 ? a.t_b : a.l);
+    }
     const int kq = max(0, min(p.t1, a.kg) - p.t0);
     const int kf = p.t1 - max(p.t0, a.kg);
     const int vq = max(0, min(p.t1, a.vg) - p.t0);

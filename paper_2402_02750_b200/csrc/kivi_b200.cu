@@ -493,12 +493,20 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         return fail(KIVI_ERR_USAGE, "internal: fused append outside its route");
     const int64_t t_first = nfull * fast::BSUB;
     const int tsub = latency_bound ? tsub_small : tsub_env;
-    const int64_t n_sub = nfull + ceil_div(h->l - t_first, tsub);
+    // few-unit route: the residual window [floor32(vg), l) in rsub-token items
+    static const int rsub_env = env_int("KIVI_RES_SUB", 32) / 32 * 32;
+    const int rsub = (latency_bound && l_app < 0 && rsub_env > 0) ? rsub_env : 0;
+    const int64_t t_b = rsub ? (h->vg() / 32) * 32 : h->l;
+    const int64_t n_a = ceil_div(t_b - t_first, tsub);
+    const int64_t n_b = rsub ? ceil_div(h->l - t_b, rsub) : 0;
+    const int64_t n_sub = nfull + n_a + n_b;
     if (h->l >= (1LL << 30) || U * n_sub >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
     // partials sized for the reserved capacity: growing them mid-decode would
     // cudaFree (a device-wide sync) inside a serving loop
-    const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, std::min(tsub_env, tsub_small)) + 2);
+    const int64_t n_sub_cap = std::max<int64_t>(
+        n_sub, ceil_div(h->cap, std::min(tsub_env, tsub_small)) + 2 +
+                   (rsub_env > 0 ? ceil_div(h->cfg.residual_length + 32, std::max(rsub_env, 32)) : 0));
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
     if (rc) return rc;
     rc = ensure(&h->part_ml, &h->ml_cap, U * n_sub_cap);
@@ -585,6 +593,9 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.k_first = (int)nfull;
         a.t_first = (int)t_first;
         a.sub = tsub;
+        a.sub_b = rsub;
+        a.n_a = (int)n_a;
+        a.t_b = (int)t_b;
         a.n_per_unit = (int)(n_sub - nfull);
         a.n_items = (int)(U * a.n_per_unit);
         a.tk = tk;
