@@ -495,7 +495,9 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int tsub = latency_bound ? tsub_small : tsub_env;
     // few-unit route: the residual window [floor32(vg), l) in rsub-token items
     static const int rsub_env = env_int("KIVI_RES_SUB", 32) / 32 * 32;
-    static const int rsub_body = env_int("KIVI_RES_SUB_BODY", 0);
+    // (KIVI_RES_SUB_BODY=1: on the body route too; measured slower on C2,
+    // within noise on C5)
+    static const bool rsub_body = env_int("KIVI_RES_SUB_BODY", 0) != 0;
     const int rsub = ((latency_bound || rsub_body) && l_app < 0 && rsub_env > 0) ? rsub_env : 0;
     const int64_t t_b = rsub ? (h->vg() / 32) * 32 : h->l;
     const int64_t n_a = ceil_div(t_b - t_first, tsub);
