@@ -729,6 +729,24 @@ __device__ __forceinline__ ItemPlan plan_item(const FastArgs& a, int item) {
     return p;
 }
 
+// L2 bulk prefetch of an item's fp32 residual rows (keys [max(t0, kg), t1),
+// values [max(t0, vg), t1) in the ring); lane 0 only.
+__device__ __forceinline__ void prefetch_item_rows(const FastArgs& a, const ItemPlan& p) {
+    const CacheDev& c = a.c;
+    const int kf0 = max(p.t0, a.kg);
+    if (p.t1 > kf0)
+        bulk_prefetch_l2(c.kring + p.u * c.ring_ustride + (int64_t)(kf0 - a.kg) * D,
+                         (uint32_t)(p.t1 - kf0) * D * 4);
+    const int vf0 = max(p.t0, a.vg);
+    if (p.t1 > vf0) {
+        const float* ring = c.vring + p.u * c.ring_ustride;
+        const int r0 = vf0 % c.R, n = p.t1 - vf0;
+        const int n1 = min(n, c.R - r0);
+        bulk_prefetch_l2(ring + (int64_t)r0 * D, (uint32_t)n1 * D * 4);
+        if (n > n1) bulk_prefetch_l2(ring, (uint32_t)(n - n1) * D * 4);
+    }
+}
+
 struct JobDesc {
     int kind;
     int ts;  // first token
@@ -884,21 +902,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     // when the item's first job is issued, turning the chain's HBM round trips
     // into L2 hits.  Used on the few-unit route (C1: 22.2 -> 21.2 us); beside
     // the body kernel it costs more than it saves (C2 248 -> 258 us).
-    auto prefetch_rows = [&](const ItemPlan& p) {
-        const CacheDev& c = a.c;
-        const int kf0 = max(p.t0, a.kg);
-        if (p.t1 > kf0)
-            bulk_prefetch_l2(c.kring + p.u * c.ring_ustride + (int64_t)(kf0 - a.kg) * D,
-                             (uint32_t)(p.t1 - kf0) * D * 4);
-        const int vf0 = max(p.t0, a.vg);
-        if (p.t1 > vf0) {
-            const float* ring = c.vring + p.u * c.ring_ustride;
-            const int r0 = vf0 % c.R, n = p.t1 - vf0;
-            const int n1 = min(n, c.R - r0);
-            bulk_prefetch_l2(ring + (int64_t)r0 * D, (uint32_t)n1 * D * 4);
-            if (n > n1) bulk_prefetch_l2(ring, (uint32_t)(n - n1) * D * 4);
-        }
-    };
+    auto prefetch_rows = [&](const ItemPlan& p) { prefetch_item_rows(a, p); };
     int f_item = first_item(), f_job = 0;
     ItemPlan f_plan{};
     if (!(APP && a.gbar)) enter_unit(f_item);
