@@ -115,12 +115,19 @@ struct kivi_cache {
     int64_t stats_cap = 0;
     int fast_per_sm[9][4] = {};
     // staging for _host calls
-    float* st_q = nullptr;
-    float* st_k = nullptr;
-    float* st_v = nullptr;
-    float* st_out = nullptr;
-    float* st_w = nullptr;
-    int64_t st_cap_q = 0, st_cap_out = 0, st_cap_k = 0, st_cap_v = 0, st_cap_w = 0;
+    // host-path staging, double-buffered: call i uploads into stg[i & 1]
+    // while call i-1's kernels may still read stg[(i-1) & 1]
+    struct HostStage {
+        float* q = nullptr;
+        float* k = nullptr;
+        float* v = nullptr;
+        float* out = nullptr;
+        float* w = nullptr;
+        int64_t cap_q = 0, cap_out = 0, cap_k = 0, cap_v = 0, cap_w = 0;
+        cudaEvent_t in_free = nullptr;   // staged inputs consumed by the kernels
+        cudaEvent_t out_free = nullptr;  // staged result copied to the host
+    } stg[2];
+    int stg_i = 0;
     double* xfer = nullptr;  // export/import staging
     int64_t xfer_cap = 0;
     // host-buffer path: inputs are uploaded on a private copy stream so the
@@ -131,14 +138,12 @@ struct kivi_cache {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* work = nullptr;  // body kernels' dynamic item counters: a ring of WORK_SLOTS
     int64_t work_seq = 0; // body launches so far (slot = work_seq % WORK_SLOTS)
-    cudaEvent_t ev_in_free = nullptr;   // staged inputs consumed by the kernels
     cudaEvent_t ev_h2d_done = nullptr;  // staged inputs uploaded
     unsigned long long* small_sync = nullptr;  // [1 + n_units] single-launch decode counters
     unsigned long long small_gbar = 0;         // cumulative grid-barrier target
     unsigned int small_units = 0;              // cumulative per-unit item target
     cudaStream_t d2h = nullptr;         // result copies of the host path
     cudaEvent_t ev_out_ready = nullptr; // staged result written by the kernels
-    cudaEvent_t ev_out_free = nullptr;  // staged result copied to the host
 
     // profiling
     bool profile = false;
@@ -894,11 +899,15 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     cudaFree(h->part_ml);
     cudaFree(h->scratch);
     cudaFree(h->stats);
-    cudaFree(h->st_q);
-    cudaFree(h->st_k);
-    cudaFree(h->st_v);
-    cudaFree(h->st_out);
-    cudaFree(h->st_w);
+    for (auto& sg : h->stg) {
+        cudaFree(sg.q);
+        cudaFree(sg.k);
+        cudaFree(sg.v);
+        cudaFree(sg.out);
+        cudaFree(sg.w);
+        if (sg.in_free) cudaEventDestroy(sg.in_free);
+        if (sg.out_free) cudaEventDestroy(sg.out_free);
+    }
     cudaFree(h->xfer);
     if (h->h2d) cudaStreamDestroy(h->h2d);
     if (h->side) cudaStreamDestroy(h->side);
@@ -908,8 +917,6 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     if (h->small_sync) cudaFree(h->small_sync);
     if (h->d2h) cudaStreamDestroy(h->d2h);
     if (h->ev_out_ready) cudaEventDestroy(h->ev_out_ready);
-    if (h->ev_out_free) cudaEventDestroy(h->ev_out_free);
-    if (h->ev_in_free) cudaEventDestroy(h->ev_in_free);
     if (h->ev_h2d_done) cudaEventDestroy(h->ev_h2d_done);
     for (auto& ev : h->events) {
         cudaEventDestroy(ev.first);
@@ -1187,24 +1194,34 @@ kivi_status kivi_prefill_host(kivi_cache* h, const float* keys, const float* val
     return KIVI_OK;
 }
 
-static kivi_status stage_rows(kivi_cache* h, int64_t qpk, int64_t wlen) {
+// The staging set for this host-path call (alternating), sized for it.  The
+// weights buffer is sized for the reserved capacity so a growing context does
+// not reallocate it every call (a cudaFree synchronises the device).
+static kivi_status stage_rows(kivi_cache* h, int64_t qpk, int64_t wlen, kivi_cache::HostStage** out) {
     const int64_t U = h->n_units, d = h->cfg.head_dim;
     kivi_status rc;
     if (!h->h2d) {
         KIVI_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
-        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_in_free, cudaEventDisableTiming));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_h2d_done, cudaEventDisableTiming));
-        KIVI_CUDA(cudaEventRecord(h->ev_in_free, h->h2d));  // nothing staged yet
         KIVI_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
         KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_out_ready, cudaEventDisableTiming));
-        KIVI_CUDA(cudaEventCreateWithFlags(&h->ev_out_free, cudaEventDisableTiming));
-        KIVI_CUDA(cudaEventRecord(h->ev_out_free, h->d2h));  // nothing to copy yet
+        for (auto& sg : h->stg) {
+            KIVI_CUDA(cudaEventCreateWithFlags(&sg.in_free, cudaEventDisableTiming));
+            KIVI_CUDA(cudaEventRecord(sg.in_free, h->h2d));  // nothing staged yet
+            KIVI_CUDA(cudaEventCreateWithFlags(&sg.out_free, cudaEventDisableTiming));
+            KIVI_CUDA(cudaEventRecord(sg.out_free, h->d2h));  // nothing to copy yet
+        }
     }
-    if ((rc = ensure(&h->st_q, &h->st_cap_q, U * qpk * d))) return rc;
-    if ((rc = ensure(&h->st_out, &h->st_cap_out, U * qpk * d))) return rc;
-    if ((rc = ensure(&h->st_k, &h->st_cap_k, U * d))) return rc;
-    if ((rc = ensure(&h->st_v, &h->st_cap_v, U * d))) return rc;
-    if (wlen > 0 && (rc = ensure(&h->st_w, &h->st_cap_w, wlen))) return rc;
+    kivi_cache::HostStage& sg = h->stg[h->stg_i];
+    h->stg_i ^= 1;
+    if ((rc = ensure(&sg.q, &sg.cap_q, U * qpk * d))) return rc;
+    if ((rc = ensure(&sg.out, &sg.cap_out, U * qpk * d))) return rc;
+    if ((rc = ensure(&sg.k, &sg.cap_k, U * d))) return rc;
+    if ((rc = ensure(&sg.v, &sg.cap_v, U * d))) return rc;
+    if (wlen > 0 &&
+        (rc = ensure(&sg.w, &sg.cap_w, std::max<int64_t>(wlen, U * qpk * (h->cap + 1)))))
+        return rc;
+    *out = &sg;
     return KIVI_OK;
 }
 
@@ -1212,18 +1229,19 @@ kivi_status kivi_append_host(kivi_cache* h, const float* t_k, const float* t_v, 
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
     if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
     DeviceGuard g(h->device);
-    kivi_status rc = stage_rows(h, 1, 0);
+    kivi_cache::HostStage* sg = nullptr;
+    kivi_status rc = stage_rows(h, 1, 0, &sg);
     if (rc) return rc;
     cudaStream_t st = S(stream);
     const size_t bytes = sizeof(float) * (size_t)(h->n_units * h->cfg.head_dim);
-    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_in_free, 0));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, bytes, cudaMemcpyHostToDevice, h->h2d));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, bytes, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, sg->in_free, 0));
+    KIVI_CUDA(cudaMemcpyAsync(sg->k, t_k, bytes, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(sg->v, t_v, bytes, cudaMemcpyHostToDevice, h->h2d));
     KIVI_CUDA(cudaEventRecord(h->ev_h2d_done, h->h2d));
     KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_h2d_done, 0));
-    rc = kivi_append(h, h->st_k, h->st_v, stream);
+    rc = kivi_append(h, sg->k, sg->v, stream);
     if (rc) return rc;
-    KIVI_CUDA(cudaEventRecord(h->ev_in_free, st));
+    KIVI_CUDA(cudaEventRecord(sg->in_free, st));
     return KIVI_OK;
 }
 
@@ -1236,33 +1254,36 @@ kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, 
     DeviceGuard g(h->device);
     const int64_t U = h->n_units, d = h->cfg.head_dim;
     const int64_t wlen = weights ? U * q_per_kv * (h->l + 1) : 0;
-    kivi_status rc = stage_rows(h, q_per_kv, wlen);
+    kivi_cache::HostStage* sg = nullptr;
+    kivi_status rc = stage_rows(h, q_per_kv, wlen, &sg);
     if (rc) return rc;
     cudaStream_t st = S(stream);
-    // upload on the copy stream once the previous call's kernels consumed the staging
-    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_in_free, 0));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_q, t_q, sizeof(float) * U * q_per_kv * d,
+    // upload on the copy stream once the kernels of the call that last used
+    // this staging set (two calls ago) consumed it: it overlaps the previous
+    // call's kernels
+    KIVI_CUDA(cudaStreamWaitEvent(h->h2d, sg->in_free, 0));
+    KIVI_CUDA(cudaMemcpyAsync(sg->q, t_q, sizeof(float) * U * q_per_kv * d,
                               cudaMemcpyHostToDevice, h->h2d));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_k, t_k, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
-    KIVI_CUDA(cudaMemcpyAsync(h->st_v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(sg->k, t_k, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
+    KIVI_CUDA(cudaMemcpyAsync(sg->v, t_v, sizeof(float) * U * d, cudaMemcpyHostToDevice, h->h2d));
     KIVI_CUDA(cudaEventRecord(h->ev_h2d_done, h->h2d));
     KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_h2d_done, 0));
-    // the previous call's result copy must have left the staging buffers
-    KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_out_free, 0));
-    rc = kivi_decode(h, h->st_q, h->st_k, h->st_v, q_per_kv, h->st_out, weights ? h->st_w : nullptr,
+    // that call's result copy must have left this set's output buffers
+    KIVI_CUDA(cudaStreamWaitEvent(st, sg->out_free, 0));
+    rc = kivi_decode(h, sg->q, sg->k, sg->v, q_per_kv, sg->out, weights ? sg->w : nullptr,
                      scale_logits, stream);
     if (rc) return rc;
-    KIVI_CUDA(cudaEventRecord(h->ev_in_free, st));
+    KIVI_CUDA(cudaEventRecord(sg->in_free, st));
     // result copy on the cache's own stream, so the next layer's kernels on
     // `stream` do not queue behind it (kivi_host_join orders `stream` after it)
     KIVI_CUDA(cudaEventRecord(h->ev_out_ready, st));
     KIVI_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_out_ready, 0));
-    KIVI_CUDA(cudaMemcpyAsync(out, h->st_out, sizeof(float) * U * q_per_kv * d,
+    KIVI_CUDA(cudaMemcpyAsync(out, sg->out, sizeof(float) * U * q_per_kv * d,
                               cudaMemcpyDeviceToHost, h->d2h));
     if (weights)
-        KIVI_CUDA(cudaMemcpyAsync(weights, h->st_w, sizeof(float) * wlen, cudaMemcpyDeviceToHost,
+        KIVI_CUDA(cudaMemcpyAsync(weights, sg->w, sizeof(float) * wlen, cudaMemcpyDeviceToHost,
                                   h->d2h));
-    KIVI_CUDA(cudaEventRecord(h->ev_out_free, h->d2h));
+    KIVI_CUDA(cudaEventRecord(sg->out_free, h->d2h));
     return KIVI_OK;
 }
 
@@ -1270,7 +1291,7 @@ kivi_status kivi_host_join(kivi_cache* h, void* stream) {
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
     if (!h->d2h) return KIVI_OK;  // no host-path call yet
     DeviceGuard g(h->device);
-    KIVI_CUDA(cudaStreamWaitEvent(S(stream), h->ev_out_free, 0));
+    for (auto& sg : h->stg) KIVI_CUDA(cudaStreamWaitEvent(S(stream), sg.out_free, 0));
     return KIVI_OK;
 }
 
