@@ -484,7 +484,20 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
     // hold the fp32 residual rows.  One partial slot per item.
     static const int tsub_env = std::max(32, std::min(fast::SUB, env_int("KIVI_TAIL_SUB", 256)) / 32 * 32);
-    static const int tsub_small = std::max(32, std::min(fast::SUB, env_int("KIVI_SMALL_SUB", 64)) / 32 * 32);
+    // few-unit route item size: KIVI_SMALL_SUB, or (0, default) sized so the
+    // items below the residual window about fill the resident warps once
+    // (C1: 32 units x 3968 tokens / 1776 warps -> 96 tokens; 64 measured
+    // 18.3 us, 96 16.2 us, 128 18.0 us)
+    static const int tsub_small_env = env_int("KIVI_SMALL_SUB", 0);
+    static const int tsub_small_min = 32;
+    const int64_t res_warps = (int64_t)num_sms() * 3 * fast::WARPS;  // tail kernel: 3 CTAs / SM
+    const int tsub_small =
+        tsub_small_env > 0
+            ? (int)std::max<int64_t>(32, std::min<int64_t>(fast::SUB, tsub_small_env) / 32 * 32)
+            : (int)std::min<int64_t>(fast::SUB,
+                                     std::max<int64_t>(tsub_small_min,
+                                                       ceil_div(ceil_div(U * std::max<int64_t>(h->vg(), 1),
+                                                                         res_warps), 32) * 32));
     // Few units (e.g. one sequence's 32 heads): 256-token body items leave
     // most warps idle and the per-unit residual item becomes the critical
     // path, so every token goes through tsub-token items instead.
@@ -513,7 +526,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // partials sized for the reserved capacity: growing them mid-decode would
     // cudaFree (a device-wide sync) inside a serving loop
     const int64_t n_sub_cap = std::max<int64_t>(
-        n_sub, ceil_div(h->cap, std::min(tsub_env, tsub_small)) + 2 +
+        n_sub, ceil_div(h->cap, std::min(tsub_env, tsub_small_min)) + 2 +
                    (rsub_env > 0 ? ceil_div(h->cfg.residual_length + 32, std::max(rsub_env, 32)) : 0));
     kivi_status rc = ensure(&h->part_o, &h->part_cap, U * n_sub_cap * fast::D);
     if (rc) return rc;
