@@ -157,7 +157,7 @@ def attend_kernel_name(qpk, units, ctx, sms=148):
         return ("kivi_b200::gqa_tc::attend_gqa_tc_kernel (tensor cores) + "
                 "gqa::attend_gqa_kernel (residual items, side stream)")
     if units * -(-ctx // 256) < 4 * sms:
-        return "kivi_b200::fast::attend_tail_kernel (few-unit route, 64-token items)"
+        return "kivi_b200::fast::attend_tail_kernel (few-unit route, short items)"
     return ("kivi_b200::fast::attend_body_kernel + attend_tail_kernel (concurrent, one stream, "
             "programmatic launch)")
 
