@@ -247,10 +247,15 @@ using WSB = WarpSmemBody;
 // ===================== shared compute bodies ===============================
 
 // q row (staged by TMA) -> q * scale * log2(e) table.
-__device__ __forceinline__ void load_q_table(const float* qraw, float* qq, float qscale, int lane) {
+// The table holds (q * qscale) * ksc: the key loops' per-channel multiplier
+// (q s ksc) is then one multiply, and the logits' bias / fp32-row dots are
+// scaled back by 1 / ksc once per token.
+__device__ __forceinline__ void load_q_table(const float* qraw, float* qq, float qscale, float ksc,
+                                             int lane) {
     const float4 qv = reinterpret_cast<const float4*>(qraw)[lane];
     reinterpret_cast<float4*>(qq)[lane] =
-        make_float4(qv.x * qscale, qv.y * qscale, qv.z * qscale, qv.w * qscale);
+        make_float4((qv.x * qscale) * ksc, (qv.y * qscale) * ksc, (qv.z * qscale) * ksc,
+                    (qv.w * qscale) * ksc);
     __syncwarp();
 }
 
@@ -288,8 +293,8 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
                     pr_n = *reinterpret_cast<const float4*>(pairs + ci * 16);
                     qv_n = *reinterpret_cast<const float2*>(qq + 2 * ci);
                 }
-                const float m0 = qv.x * ksc * (pr.y - pr.x);
-                const float m1 = qv.y * ksc * (pr.w - pr.z);
+                const float m0 = qv.x * (pr.y - pr.x);
+                const float m1 = qv.y * (pr.w - pr.z);
                 bias = fmaf(qv.x, pr.x, bias);
                 bias = fmaf(qv.y, pr.z, bias);
                 PB::fma_word(acc, cw.x, m0);
@@ -307,7 +312,7 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
                 const uint4 cw = *reinterpret_cast<const uint4*>(codes + ci * 16);
                 const float2 pr = *reinterpret_cast<const float2*>(pairs + ci * 8);
                 const float qv = qq[ci];
-                const float m0 = qv * ksc * (pr.y - pr.x);
+                const float m0 = qv * (pr.y - pr.x);
                 bias = fmaf(qv, pr.x, bias);
                 PB::fma_word(acc, cw.x, m0);
                 PB::fma_word(acc + 4, cw.y, m0);
@@ -346,7 +351,7 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
         float lg[TPL];
 #pragma unroll
         for (int i = 0; i < TPL; ++i)
-            lg[i] = fmaf(sum[i], unscale_pos(PB::epos((TPL * b + i) % PB::TPW)), bias);
+            lg[i] = fmaf(sum[i], unscale_pos(PB::epos((TPL * b + i) % PB::TPW)), bias * (1.0f / ksc));
         float* dst = probs_dst + tl * 32 + TPL * b;
         if constexpr (TPL == 4)
             *reinterpret_cast<float4*>(dst) = make_float4(lg[0], lg[1], lg[2], lg[3]);
@@ -359,7 +364,8 @@ __device__ __forceinline__ void kq_tiles_to_logits(uint8_t* slot, const float* q
 // (lane owns channels 4*lane..4*lane+3), then one xor-16 step and a
 // reduce-scatter over 16 lanes, after which lane r (< 16) holds row r.
 __device__ __forceinline__ void kf_rows_to_logits(const uint8_t* slot, const float* qq,
-                                                  float* probs_dst, int n, int lane) {
+                                                  float* probs_dst, int n, float inv_ksc,
+                                                  int lane) {
     const float4 qa = reinterpret_cast<const float4*>(qq)[lane];
     float part[F_ROWS];
 #pragma unroll
@@ -382,7 +388,7 @@ __device__ __forceinline__ void kf_rows_to_logits(const uint8_t* slot, const flo
             part[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
         }
     }
-    if (lane < n) probs_dst[lane] = part[0];
+    if (lane < n) probs_dst[lane] = part[0] * inv_ksc;
 }
 
 // Softmax over the item's logits (in place, log2 domain); returns (max, sum).
@@ -665,7 +671,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
 #pragma unroll 1
         for (int jk = 0; jk < NKJ; ++jk) {
             uint8_t* slot = wait_slot();
-            if (jk == 0) load_q_table(qraw, qq, a.qscale, lane);
+            if (jk == 0) load_q_table(qraw, qq, a.qscale, ksc, lane);
             kq_tiles_to_logits<B>(slot, qq, probs + jk * PB::KQ_TILES * 32, PB::KQ_TILES, ksc,
                                   lane);
             release_slot();
@@ -943,12 +949,12 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
         const int nk = p.nkq + p.nkf;
         for (int j = 0; j < nk; ++j) {
             uint8_t* slot = wait_slot();
-            if (j == 0) load_q_table(qraw, qq, a.qscale, lane);
+            if (j == 0) load_q_table(qraw, qq, a.qscale, ksc, lane);
             const JobDesc jd = job_of<B>(a, p, j);
             if (jd.kind == KQ)
                 kq_tiles_to_logits<B>(slot, qq, probs + (jd.ts - p.t0), jd.n, ksc, lane);
             else
-                kf_rows_to_logits(slot, qq, probs + (jd.ts - p.t0), jd.n, lane);
+                kf_rows_to_logits(slot, qq, probs + (jd.ts - p.t0), jd.n, 1.0f / ksc, lane);
             release_slot();
         }
         const float2 ml = softmax_item(
