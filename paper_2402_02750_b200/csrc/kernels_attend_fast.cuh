@@ -58,6 +58,10 @@ constexpr int KQ_UNROLL = KIVI_KQ_UNROLL;
 
 // w >> K on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF): the body
 // kernel is ALU-bound on the code extraction, the FMA pipe has headroom.
+#ifndef KIVI_COMBINE_UNROLL
+#define KIVI_COMBINE_UNROLL 8
+#endif
+constexpr int COMBINE_UNROLL = KIVI_COMBINE_UNROLL;  // K5 partial loop (x2 loads)
 #ifndef KIVI_VQ_UNROLL
 #define KIVI_VQ_UNROLL 1
 #endif
@@ -1024,7 +1028,7 @@ __device__ __forceinline__ void combine_row(const float* __restrict__ part_o,
         __syncthreads();
         const int nk = min(128, n_sub - k0);
         int i = 0;
-#pragma unroll 4
+#pragma unroll COMBINE_UNROLL
         for (; i + 1 < nk; i += 2) {
             o = fmaf(part_o[(ml0 + (int64_t)(k0 + i) * ms) * D + c], sw[i], o);
             o1 = fmaf(part_o[(ml0 + (int64_t)(k0 + i + 1) * ms) * D + c], sw[i + 1], o1);
