@@ -153,6 +153,8 @@ struct FastArgs {
     int* work;          // body kernel: dynamic item counter (zero at launch)
     int* work_clear;    // body kernel: a later launch's counter, zeroed here
     int prefetch;       // tail kernel: L2-prefetch each item's fp32 rows
+    int tail_last;      // one-stream order body -> tail (tail needs only the append,
+                        // which finished before the body started)
     // tail kernel, two item sizes per unit (few-unit route): items
     // [0, n_a) are `sub` tokens from t_first up to t_b, items [n_a, n_per_unit)
     // are sub_b tokens from t_b (the residual window's fp32 rows in short
@@ -604,6 +606,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     const int nper = a.n_per_unit;
     const float ksc = TWO_POW_64 / (float)((1 << B) - 1);
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.work_clear) *a.work_clear = 0;
+    if (a.tail_last) pdl_trigger();  // the residual-window kernel may follow at once
 
     // Items are taken dynamically (atomic counter), one item ahead of use, so
     // CTAs that start late — e.g. after a concurrently running tail kernel
@@ -851,8 +854,8 @@ __device__ __forceinline__ void issue_job(const FastArgs& a, int u, const JobDes
 template <int B, int NW = WARPS, bool APP = false>
 __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
     using PB = P<B>;
-    pdl_wait();     // the append before it (programmatic launch, few-unit route)
-    pdl_trigger();  // ... and the combine after it
+    if (!a.tail_last) pdl_wait();  // the append before it (programmatic launch)
+    pdl_trigger();                  // ... and the launch after it
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* wbase = smem_raw + warp * WS2::STRIDE;
@@ -996,6 +999,7 @@ __global__ void __launch_bounds__(NW * 32, 3) attend_tail_kernel(FastArgs a) {
             release_slot();
         }
     }
+    if (a.tail_last) pdl_wait();  // finish only after the body kernel before it
 }
 
 // K5 row merge, one 128-thread block per output row (thread c = channel c):

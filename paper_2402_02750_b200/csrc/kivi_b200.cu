@@ -604,6 +604,10 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const bool one_stream = use_pdl && nfull > 0 && has_tail && l_app < 0 && !tail_warp_ctas &&
                             !(B == 2 && mha_tc);
     cudaStream_t tail_st = (tail_side && nfull > 0 && !one_stream) ? h->side : st;
+    static const int tail_last_env = env_int("KIVI_TAIL_LAST", 0);
+    const bool tail_last = one_stream && tail_last_env;
+    fast::FastArgs a_tail{};
+    bool tail_deferred = false;
     if (has_tail) {
         // Tail items (residual fp32 tokens, latency-bound) with 2 CTAs per SM,
         // concurrently with the ALU-bound body kernel.
@@ -623,7 +627,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.tv = tv;
         a.l_app = (int)l_app;
         a.prefetch = latency_bound ? 1 : 0;
-        if (nfull > 0 && tail_st != st && tail_warp_ctas && l_app < 0) {
+        if (tail_last) {
+            // launched after the body (below)
+            a_tail = a;
+            a_tail.tail_last = 1;
+            tail_deferred = true;
+        } else if (nfull > 0 && tail_st != st && tail_warp_ctas && l_app < 0) {
             // one-warp CTAs beside the body kernel: every tail item its own warp
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * tail_warp_ctas,
                                                    a.n_items);
@@ -643,9 +652,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             else
                 fast::attend_tail_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem, tail_st>>>(a);
         }
-        KIVI_LAUNCHED();
-        if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
-        h->total_launches++;
+        if (!tail_deferred) {
+            KIVI_LAUNCHED();
+            if (tail_st != st) KIVI_CUDA(cudaEventRecord(h->ev_join, tail_st));
+            h->total_launches++;
+        }
     }
     if (nfull > 0) {
         a.l_app = -1;
@@ -664,7 +675,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         } else {
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
                                                    ceil_div(a.n_items, fast::WARPS));
-            if (one_stream)
+            if (tail_deferred) {
+                // body first (normal launch: the append is complete), then the
+                // residual-window kernel as its programmatic dependent
+                a.tail_last = 1;
+                fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
+            } else if (one_stream)
                 KIVI_CUDA(launch_pdl(fast::attend_body_kernel<B>, dim3((unsigned)grid),
                                      dim3(fast::WARPS * 32), (size_t)smem_body, st, a));
             else
@@ -672,6 +688,14 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         }
         KIVI_LAUNCHED();
         h->total_launches++;
+        if (tail_deferred) {
+            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][1],
+                                                   ceil_div(a_tail.n_items, fast::WARPS));
+            KIVI_CUDA(launch_pdl(fast::attend_tail_kernel<B>, dim3((unsigned)grid),
+                                 dim3(fast::WARPS * 32), (size_t)smem, st, a_tail));
+            KIVI_LAUNCHED();
+            h->total_launches++;
+        }
     }
     if (has_tail && tail_st != st) KIVI_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
     if (h->prof_now) {
