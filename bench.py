@@ -148,9 +148,6 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-PROF_STRIDE = 4   # time every 4th attend launch of each cache (bench loop below)
-
-
 def attend_kernel_name(qpk, units, ctx, sms=148):
     """The attend launch the roofline times (library routing, kivi_b200.cu)."""
     if qpk > 1:
@@ -169,10 +166,75 @@ def dist_setup():
     return world, rank, local
 
 
+def self_launch(n):
+    """`bench.py --gpus N` outside torchrun: re-runs this command as N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1 and
+    returns its exit code.  NCCL logs (NCCL_DEBUG=INFO unless set) go to
+    gpurun_out/nccl.<host>.<pid>.log so stdout keeps rank 0's one JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    if "NCCL_DEBUG_FILE" not in env:
+        logdir = os.path.join(ROOT, "gpurun_out")
+        os.makedirs(logdir, exist_ok=True)
+        env["NCCL_DEBUG_FILE"] = os.path.join(logdir, "nccl.%h.%p.log")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def workload_config(args, world, rank=0, free_bytes=None):
+    """The workload both arms report (same keys, same values): BASELINE config,
+    per-GPU units, scaling mode and, when a rank's share does not fit its HBM,
+    the largest power-of-two batch that does (C4 on one GPU)."""
+    from paper_2402_02750_b200.sharding import partition_units
+    layers, heads, batch, ctx, bits, qpk, desc = CONFIGS[args.config]
+    if args.layers:
+        layers = args.layers
+    if args.bits:
+        bits = args.bits
+        desc = desc.replace("2-bit", f"{bits}-bit")
+    scaling = args.scaling or ("strong" if args.config in ("c4", "c5") else "weak")
+    if scaling == "strong":
+        U = len(partition_units(batch, heads, world, rank))  # fixed global batch
+        global_batch = batch
+    else:
+        U = batch * heads  # every rank serves its own batch
+        global_batch = batch * world
+    steps, warmup = args.steps, args.warmup
+    capacity_note = None
+    per_unit = state_bytes_per_unit(ctx + steps + warmup + R, bits, layers) + 2 * 4 * D * ctx
+    if free_bytes is not None and U * per_unit > 0.85 * free_bytes:
+        b_rank = max(1, U // heads)
+        while b_rank > 1 and b_rank * heads * per_unit > 0.85 * free_bytes:
+            b_rank //= 2
+        capacity_note = (f"{U // heads} sequences/GPU need {U * per_unit / 1e9:.0f} GB of "
+                         f"state > {free_bytes / 1e9:.0f} GB free: timed {b_rank} sequences/GPU")
+        U = b_rank * heads
+        global_batch = b_rank * world
+        scaling = "weak"
+    cfg = {"workload": desc, "name": args.config, "layers": layers, "kv_heads": heads,
+           "batch_per_gpu": global_batch / world, "global_batch": global_batch, "ctx": ctx,
+           "bits": bits, "group_size": G, "residual": R, "head_dim": D, "q_per_kv": qpk,
+           "units_per_layer_per_gpu": U, "capacity_limited": capacity_note,
+           "l_timed": [ctx - steps + 1, ctx],
+           "parallelism": f"dp{world} ({scaling}; units sharded by (batch, kv-head), "
+                          "no collective)"}
+    return cfg, U, scaling
+
+
+# ---- the reference / oracle legs (the only code here that executes oracle/) --
+
 def cpu_reference_sample(cfg_name, steps, warmup, threads, units=None, bits=0):
     """Times the REFERENCE decode_attention (oracle/_ref, compiled from the
     reference sources) on a bounded sample of the workload's units; returns
-    (unit-steps per second, description, kind)."""
+    (unit-steps per second, description, kind, measured seconds, units)."""
     layers, heads, batch, ctx, cbits, qpk, _ = CONFIGS[cfg_name]
     bits = bits or cbits
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -185,39 +247,117 @@ def cpu_reference_sample(cfg_name, steps, warmup, threads, units=None, bits=0):
     rate = units * steps / secs  # unit-steps / s (each = one reference decode_attention call)
     desc = (f"{units} units x {steps} timed decode steps (after {warmup} warm-up) at l={l0}.."
             f"{l0 + warmup + steps}, reference decode_attention per unit (append+attend), "
-            f"{threads} threads; extrapolated to {layers * heads * batch * qpk} unit-steps/step")
-    return rate, desc, "reference"
+            f"{threads} threads, {secs:.2f} s measured; extrapolated linearly to "
+            f"{layers * heads * batch * qpk} unit-steps/step")
+    return rate, desc, "reference", secs, units
+
+
+def reference_parity_sample(bits, qpk, prompts, seq, outs, states):
+    """Replays the sampled units of layer 0 through the reference itself
+    (oracle/_ref: prefill, append_token per step, decode_attention on the last
+    one, per query head on a state copy) and compares with what the timed GPU
+    path produced: the exported state bit-exactly, the last output by rel-L2.
+    prompts: {unit: (K, V)}; seq: [(k[U,d], v[U,d], q[U,qpk,d])] per step;
+    outs: {unit: [qpk, d]} last-step outputs; states: {unit: exported state}."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import Ref, rel_l2
+    if not Ref.available():
+        return None
+    ref = Ref()
+
+    def one(u):
+        K, V = prompts[u]
+        r = ref.unit(bits, G, R, D)
+        r.prefill(K, V)
+        for tk, tv, _ in seq[:-1]:
+            r.append(tk[u], tv[u])
+        tk, tv, q = seq[-1]
+        heads = [r] + [r.clone() for _ in range(qpk - 1)]
+        err = 0.0
+        for h in range(qpk):
+            err = max(err, rel_l2(outs[u][h], heads[h].decode(q[u, h], tk[u], tv[u])))
+        want = r.export()
+        exact = all(np.asarray(states[u][k]).tobytes() == want[k].tobytes() for k in want)
+        return err, exact
+
+    with ThreadPoolExecutor(max_workers=len(prompts)) as ex:
+        res = list(ex.map(one, sorted(prompts)))
+    return {"units": sorted(int(u) for u in prompts), "layer": 0,
+            "checker": "reference (oracle/_ref)",
+            "steps_replayed": len(seq), "state_bit_exact": all(e for _, e in res),
+            "max_rel_l2": max(e for e, _ in res), "bar_rel_l2": 1e-5}
 
 
 def run_reference_arm(args):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    layers, heads, batch, ctx, bits, qpk, desc = CONFIGS[args.config]
-    if args.bits:
-        bits = args.bits
-        desc = desc.replace("2-bit", f"{bits}-bit")
+    world = max(world, args.gpus)
+    cfg, _, scaling = workload_config(args, world, 0, None)
+    layers, heads, qpk, bits = cfg["layers"], cfg["kv_heads"], cfg["q_per_kv"], cfg["bits"]
+    batch = cfg["global_batch"]
     threads = os.cpu_count() or 1
     # each "step" is a bounded sample: ~16 units per thread, one decode each
-    rate, sample, kind = cpu_reference_sample(args.config, args.steps, args.warmup, threads,
-                                              units=16 * threads, bits=bits)
+    rate, sample, kind, secs, units = cpu_reference_sample(args.config, args.steps, args.warmup,
+                                                           threads, units=16 * threads, bits=bits)
     unit_steps_per_step = layers * heads * batch * qpk
     step_s = unit_steps_per_step / rate
     tok_s = batch / step_s
     line = {
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32/f64 (reference CPU)", "data": "synthetic",
-        "config": {"workload": desc, "layers": layers, "kv_heads": heads, "batch": batch,
-                   "ctx": ctx, "bits": bits, "group_size": G, "residual": R, "head_dim": D,
-                   "q_per_kv": qpk},
+        "config": cfg,
+        "sampled_units": units, "sample_seconds": secs,
+        "ms_per_step_note": ("extrapolated: the full step is "
+                             f"{unit_steps_per_step} reference decode_attention calls; "
+                             f"{units} units x {args.steps} steps measured in {secs:.2f} s"),
         "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_dry(args):
+    """CPU rehearsal of the multi-rank path (gloo, no GPU): every rank takes its
+    unit shard, 'times' it, and the max over ranks is reduced; rank 0 prints the
+    JSON line.  Covered by tests/test_bench_launch.py through self_launch."""
+    import torch.distributed as dist
+    world, rank, _ = dist_setup()
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg, U, scaling = workload_config(args, world, rank, None)
+    t = 1e-3 * (1 + rank)
+    from paper_2402_02750_b200.sharding import max_over_ranks
+    t = max_over_ranks(t)
+    units = [U]
+    if world > 1:
+        units = [None] * world
+        dist.all_gather_object(units, U)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "value": None,
+                          "unit": "tokens/s", "steps": args.steps, "warmup": args.warmup,
+                          "scaling": scaling, "config": cfg, "units_per_rank": units,
+                          "max_rank_time_s": t}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def percentiles(xs):
+    ys = sorted(xs)
+    if not ys:
+        return None
+
+    def p(f):
+        return ys[min(len(ys) - 1, max(0, int(math.ceil(f * len(ys))) - 1))]
+
+    return {"p50": p(0.5), "p90": p(0.9), "p99": p(0.99), "max": ys[-1],
+            "mean": sum(ys) / len(ys), "n": len(ys)}
 
 
 def run_ours(args):
@@ -232,72 +372,17 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    layers, heads, batch, ctx, bits, qpk, desc = CONFIGS[args.config]
-    if args.layers:
-        layers = args.layers
-    if args.bits:
-        bits = args.bits
-        desc = desc.replace("2-bit", f"{bits}-bit")
-    from paper_2402_02750_b200.sharding import partition_units
-    scaling = args.scaling or ("strong" if args.config in ("c4", "c5") else "weak")
-    capacity_note = None
-    if scaling == "strong":
-        # fixed global batch, units partitioned over ranks (no collective)
-        U = len(partition_units(batch, heads, world, rank))
-        global_batch = batch
-    else:
-        # every rank serves its own batch (data-parallel replicas)
-        U = batch * heads
-        global_batch = batch * world
-    steps, warmup = args.steps, args.warmup
-    # C4 (Llama-2-13B, batch 256: 2-bit ~287 GB, 4-bit ~344 GB of state) does
-    # not fit one 180 GB B200 (SURVEY §7 hard part 5).  When a rank's share
-    # does not fit, it runs the largest power-of-two batch that does, and the
-    # line says so; at 8 GPUs (32 sequences per GPU) the full job fits.
     free, _ = torch.cuda.mem_get_info(dev)
-    per_unit = state_bytes_per_unit(ctx + steps + warmup + R, bits, layers) + 2 * 4 * D * ctx
-    if U * per_unit > 0.85 * free:
-        b_rank = max(1, U // heads)
-        while b_rank > 1 and b_rank * heads * per_unit > 0.85 * free:
-            b_rank //= 2
-        capacity_note = (f"{U // heads} sequences/GPU need {U * per_unit / 1e9:.0f} GB of "
-                         f"state > {free / 1e9:.0f} GB free: timed {b_rank} sequences/GPU")
-        U = b_rank * heads
-        global_batch = b_rank * world
-        scaling = "weak"
+    config, U, scaling = workload_config(args, world, rank, free)
+    layers, heads, ctx, bits, qpk = (config["layers"], config["kv_heads"], config["ctx"],
+                                     config["bits"], config["q_per_kv"])
+    global_batch = int(config["global_batch"])
+    steps, warmup = args.steps, args.warmup
     l0 = ctx - warmup - steps
     if l0 < 1:
         raise SystemExit("--steps + --warmup must be < ctx")
     cfg = kb.CacheConfig(bits, G, R, D)
-
-    # ---- build the state: prefill every layer on the device ----------------
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    caches = []
-    kbuf = torch.empty((U, l0, D), device=dev, dtype=torch.float32)
-    vbuf = torch.empty_like(kbuf)
-    for _ in range(layers):
-        c = kb.KVCache(cfg, U, capacity_tokens=ctx + steps + warmup + R, device=local)
-        kbuf.uniform_(-1.0, 1.0, generator=gen)
-        vbuf.uniform_(-1.0, 1.0, generator=gen)
-        c.prefill(kbuf, vbuf)
-        c.set_attend_path("auto")
-        caches.append(c)
-    del kbuf, vbuf
-    torch.cuda.synchronize()
-    torch.cuda.empty_cache()
-
-    # per-step inputs resident in HBM (a pool of 2 sets per layer, cycled)
-    pool = 2
-    qs = torch.empty((pool, layers, U, qpk, D), device=dev).uniform_(-1, 1, generator=gen)
-    ks = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
-    vs = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
-    outs = torch.empty((layers, U, qpk, D), device=dev)
-
-    def step(i):
-        p = i % pool
-        for ly in range(layers):
-            caches[ly].decode(qs[p, ly], ks[p, ly], vs[p, ly], q_per_kv=qpk, out=outs[ly])
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
@@ -313,77 +398,137 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for i in range(warmup):
-        step(i)
-    barrier()
-    # the attend kernel's launch time (roofline) comes from CUDA events the
-    # library records around it inside the timed region, on every
-    # PROF_STRIDE-th launch of each cache: the events cost host time, which
-    # latency-bound steps (C1: 38 vs 44 us/step with every launch timed)
-    # would otherwise pay in `value`
-    prof = 0 if os.environ.get("KIVI_BENCH_NOPROF") else PROF_STRIDE
+    # ---- state: prefilled on the device; rebuilt identically before each pass
+    caches = [kb.KVCache(cfg, U, capacity_tokens=ctx + steps + warmup + R, device=local)
+              for _ in range(layers)]
     for c in caches:
-        c.profile_read()
-        c.profile_enable(prof)
-    l_start = caches[0].total_tokens
-    # ---- timed region (device-resident inputs) ------------------------------
+        c.set_attend_path("auto")
+    kbuf = torch.empty((U, l0, D), device=dev, dtype=torch.float32)
+    vbuf = torch.empty_like(kbuf)
+    gen = torch.Generator(device=dev)
+    do_parity = rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_parity
+    sample_units = sorted({(i * U) // 8 + (i % 3) for i in range(8)} & set(range(U)))
+    prompts = {}
+
+    def rebuild():
+        """Every layer back to l0 tokens, from the same seeded draws."""
+        for ly in range(layers):
+            gen.manual_seed(1234 + 1000 * rank + ly)
+            kbuf.uniform_(-1.0, 1.0, generator=gen)
+            vbuf.uniform_(-1.0, 1.0, generator=gen)
+            caches[ly].prefill(kbuf, vbuf)
+            if ly == 0 and do_parity and not prompts:
+                for u in sample_units:
+                    prompts[u] = (kbuf[u].cpu().numpy(), vbuf[u].cpu().numpy())
+        torch.cuda.synchronize()
+
+    # per-step inputs resident in HBM (a pool of 2 sets per layer, cycled)
+    pool = 2
+    gen.manual_seed(99 + rank)
+    qs = torch.empty((pool, layers, U, qpk, D), device=dev).uniform_(-1, 1, generator=gen)
+    ks = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
+    vs = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
+    outs = torch.empty((layers, U, qpk, D), device=dev)
+
+    def step(j):
+        p = j % pool
+        for ly in range(layers):
+            caches[ly].decode(qs[p, ly], ks[p, ly], vs[p, ly], q_per_kv=qpk, out=outs[ly])
+
     # A state smaller than 4x L2 (C1: 18.6 MB vs 126 MB) would be served from
     # L2: then every timed step is bracketed by its own events and L2 is
     # flushed (a 2x-L2 write) between steps, outside the events.
-    stream = torch.cuda.current_stream()
     l2 = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20))
     state_total = U * state_bytes_per_unit(ctx + steps + warmup + R, bits, layers)
     flush = state_total < 4 * l2
     scratch = torch.empty((2 * l2) // 4, dtype=torch.float32, device=dev) if flush else None
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    l2_note = (f"state {state_total / 1e6:.1f} MB < 4x L2 ({l2 >> 20} MB): L2 flushed by a "
+               f"{2 * l2 >> 20} MB write between timed steps (per-step events)" if flush else
+               f"state {state_total / 1e9:.1f} GB >> {l2 >> 20} MB L2 (inputs larger than L2, "
+               "no flush)")
+
+    def timed_steps(per_step_events):
+        """K timed steps after W warm-up ones; returns (total s, per-step ms)."""
+        for j in range(warmup):
+            step(j)
         barrier()
-        if flush:
+        if per_step_events or flush:
             evs = []
             for i in range(steps):
-                scratch.fill_(float(i))
+                if flush:
+                    scratch.fill_(float(i))
                 a_ = torch.cuda.Event(enable_timing=True)
                 b_ = torch.cuda.Event(enable_timing=True)
                 a_.record(stream)
                 step(warmup + i)
                 b_.record(stream)
                 evs.append((a_, b_))
-        else:
-            e0.record(stream)
-            for i in range(steps):
-                step(warmup + i)
-            e1.record(stream)
+            barrier()
+            per = [a_.elapsed_time(b_) for a_, b_ in evs]
+            return sum(per) / 1e3, per
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            step(warmup + i)
+        e1.record(stream)
         barrier()
-    if flush:
-        elapsed = max_over_ranks(sum(a_.elapsed_time(b_) for a_, b_ in evs) / 1e3)
-    else:
-        elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    l2_note = (f"state {state_total / 1e6:.1f} MB < 4x L2 ({l2 >> 20} MB): L2 flushed by a "
-               f"{2 * l2 >> 20} MB write between timed steps (per-step events)" if flush else
-               f"state {state_total / 1e9:.1f} GB >> {l2 >> 20} MB L2 (inputs larger than L2, "
-               "no flush)")
-    kern_ms, kern_n, launches = 0.0, 0, 0
+        return e0.elapsed_time(e1) / 1e3, None
+
+    # ---- pass A: `value` (nothing recorded inside the timed region but the two
+    # events bracketing it; launches counted by the library on the host)
+    rebuild()
     for c in caches:
-        ms, n, tot = c.profile_read()
-        kern_ms += ms
-        kern_n += n   # launches timed
-        launches += tot
-        c.profile_enable(False)
-
-    # algorithmic bytes of the timed attends (l after each append), per launch
-    alg_bytes = sum(attend_bytes_per_unit(l_start + i + 1, bits, qpk) for i in range(steps))
-    alg_bytes *= U * layers
-    per_launch_bytes = alg_bytes / (steps * layers)
-    avg_launch_s = (kern_ms / 1e3) / max(kern_n, 1)
-    achieved = per_launch_bytes / avg_launch_s / 1e9 if avg_launch_s > 0 else float("nan")
-    peak, peak_src = load_peaks()
-
+        c.profile_read()
+    with ClockSampler(local) as clocks:
+        elapsed_local, per_a = timed_steps(False)
+    elapsed = max_over_ranks(elapsed_local)
+    launches = 0
+    for c in caches:
+        launches += c.profile_read()[2]
+    launches = launches * steps // (steps + warmup)  # the timed steps' share (same per step)
     tok_s = global_batch * steps / elapsed
     ms_per_step = elapsed / steps * 1e3
 
-    # ---- e2e through the C-ABI host-buffer entry point ------------------------
+    # ---- pass B: step-latency distribution (an event pair per step)
+    if per_a is None:
+        rebuild()
+        _, per_b = timed_steps(True)
+    else:
+        per_b = per_a
+    latency = percentiles(per_b)
+
+    # ---- pass C: the attend launch alone (events around every attend launch),
+    # for the roofline; not part of `value`
+    rebuild()
+    for j in range(warmup):
+        step(j)
+    barrier()
+    for c in caches:
+        c.profile_read()
+        c.profile_enable(1)
+    for i in range(steps):
+        if flush:
+            scratch.fill_(float(i))
+        step(warmup + i)
+    barrier()
+    kern_ms, kern_n = 0.0, 0
+    for c in caches:
+        ms, n, _ = c.profile_read()
+        kern_ms += ms
+        kern_n += n
+        c.profile_enable(False)
+    alg_bytes = sum(attend_bytes_per_unit(l0 + warmup + i + 1, bits, qpk) for i in range(steps))
+    alg_bytes *= U * layers
+    per_launch_bytes = alg_bytes / (steps * layers)
+    avg_launch_s = max_over_ranks((kern_ms / 1e3) / max(kern_n, 1))
+    achieved = per_launch_bytes / avg_launch_s / 1e9 if avg_launch_s > 0 else float("nan")
+    peak, peak_src = load_peaks()
+
+    # ---- pass D: e2e through the C-ABI host-buffer entry point, same window ---
     e2e = None
+    seq_used = None
+    last_out = None
     if not args.no_e2e:
         hq = torch.empty((pool, layers, U, qpk, D), dtype=torch.float32, pin_memory=True)
         hk = torch.empty((pool, layers, U, D), dtype=torch.float32, pin_memory=True)
@@ -392,47 +537,48 @@ def run_ours(args):
         hq.copy_(qs.cpu())
         hk.copy_(ks.cpu())
         hv.copy_(vs.cpu())
-        # same workload, continuing the decode: l runs past ctx.  W untimed
-        # steps first, as for the device-resident loop: a cache's first host
-        # call creates its staging buffers, copy stream and events (one-time,
-        # ~40 ms per cache).
-        e2e_steps = steps
-        for i in range(warmup):
+
+        def host_step(j):
+            p = j % pool
             for ly in range(layers):
-                caches[ly].decode_host(hq[i % pool, ly], hk[i % pool, ly], hv[i % pool, ly],
-                                       ho[ly], q_per_kv=qpk)
+                caches[ly].decode_host(hq[p, ly], hk[p, ly], hv[p, ly], ho[ly], q_per_kv=qpk)
+            for c in caches:
+                c.host_join(stream)
+            stream.synchronize()  # the step's outputs are on the host before the next
+
+        rebuild()
+        for j in range(warmup):
+            host_step(j)
         barrier()
         t0 = time.perf_counter()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        dbg = os.environ.get("KIVI_E2E_DEBUG")
-        for i in range(e2e_steps):
-            p = i % pool
-            tw = time.perf_counter()
-            for ly in range(layers):
-                caches[ly].decode_host(hq[p, ly], hk[p, ly], hv[p, ly], ho[ly], q_per_kv=qpk)
-            for c in caches:  # this step's outputs are on the host before the next
-                c.host_join(stream)
-            if dbg:
-                te = time.perf_counter() - tw
-                torch.cuda.synchronize()
-                print(f"e2e step {i}: enqueue {te * 1e3:.2f} ms, wall {(time.perf_counter() - tw) * 1e3:.2f} ms",
-                      file=sys.stderr, flush=True)
+        for i in range(steps):
+            host_step(warmup + i)
         f1.record(stream)
         barrier()
         wall = time.perf_counter() - t0
         e2e_s = max_over_ranks(max(f0.elapsed_time(f1) / 1e3, 0.0))
-        e2e = {"value": global_batch * e2e_steps / e2e_s, "unit": "tokens/s",
+        e2e = {"value": global_batch * steps / e2e_s, "unit": "tokens/s",
                "h2d_bytes_per_step": int(layers * U * (qpk + 2) * D * 4),
                "d2h_bytes_per_step": int(layers * U * qpk * D * 4),
-               "steps": e2e_steps, "wall_s": wall,
-               "path": "kivi_decode_host (C-ABI, pinned host buffers, copies in the timed region)"}
+               "steps": steps, "wall_s": wall, "l_timed": [l0 + warmup + 1, l0 + warmup + steps],
+               "path": "kivi_decode_host (C-ABI, pinned host buffers, copies in the timed "
+                       "region, host waits for every step's outputs)"}
+        seq_used = [(hk[j % pool, 0].numpy(), hv[j % pool, 0].numpy(), hq[j % pool, 0].numpy())
+                    for j in range(warmup + steps)]
+        last_out = ho[0].numpy().copy()
+    else:
+        seq_used = [(ks[j % pool, 0].cpu().numpy(), vs[j % pool, 0].cpu().numpy(),
+                     qs[j % pool, 0].cpu().numpy()) for j in range(warmup + steps)]
+        last_out = outs[0].cpu().numpy()
 
     # ---- optional NCCL all-gather of every layer's outputs ------
     gather = None
     if args.gather:
-        from paper_2402_02750_b200.sharding import gather_outputs
+        from paper_2402_02750_b200.sharding import gather_outputs, partition_units
+        batch = CONFIGS[args.config][2]
         counts = [U] * world if scaling == "weak" else \
             [len(partition_units(batch, heads, world, r)) for r in range(world)]
         for ly in range(layers):
@@ -453,19 +599,29 @@ def run_ours(args):
                   "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 rank)",
                   "note": "timed separately; not part of value"}
 
+    # ---- reference legs (rank 0, N = 1): CPU baseline + sampled-unit parity ---
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            rate, sample, kind = cpu_reference_sample(args.config, steps=min(8, steps),
-                                                      warmup=1, threads=threads,
-                                                      units=32 * threads, bits=bits)
-            step_s = layers * heads * batch * qpk / rate
-            cpu = {"value": batch / step_s, "unit": "tokens/s", "cores": threads, "kind": kind,
-                   "sample": sample}
+            rate, sample, kind, _, _ = cpu_reference_sample(
+                args.config, steps=min(8, steps), warmup=1, threads=threads,
+                units=32 * threads, bits=bits)
+            step_s = layers * heads * (global_batch // world) * qpk / rate
+            cpu = {"value": (global_batch // world) / step_s, "unit": "tokens/s",
+                   "cores": threads, "kind": kind, "sample": sample}
         except Exception as e:  # the checker is optional for our own arm
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
+        if do_parity and prompts:
+            try:
+                torch.cuda.synchronize()
+                states = {u: caches[0].export_unit(u) for u in prompts}
+                outs_u = {u: last_out[u] for u in prompts}
+                parity = reference_parity_sample(bits, qpk, prompts, seq_used, outs_u, states)
+            except Exception as e:
+                parity = {"error": str(e)}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -479,30 +635,27 @@ def run_ours(args):
             pass
 
     if rank == 0:
+        config["l_timed"] = [l0 + warmup + 1, l0 + warmup + steps]
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (uniform(-1,1) K/V/q generated on device)",
-            "config": {"workload": desc, "name": args.config, "layers": layers,
-                       "kv_heads": heads, "batch_per_gpu": global_batch / world,
-                       "global_batch": global_batch,
-                       "ctx": ctx, "bits": bits, "group_size": G, "residual": R, "head_dim": D,
-                       "q_per_kv": qpk, "units_per_layer_per_gpu": U,
-                       "capacity_limited": capacity_note,
-                       "l_timed": [l_start + 1, l_start + steps],
-                       "l2": l2_note,
-                       "parallelism": f"dp{world} ({scaling}; units sharded by "
-                                      "(batch, kv-head), no collective)"},
+            "config": config,
+            "l2": l2_note,
             "hbm_gbs_per_gpu_step": alg_bytes / elapsed / 1e9,
+            "step_latency_ms": latency,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_spec_8TBs": achieved / 8000.0,
                          "kernel": attend_kernel_name(qpk, U, ctx),
                          "bytes_per_launch": per_launch_bytes, "avg_launch_us": avg_launch_s * 1e6,
-                         "kernel_share_of_step": avg_launch_s * steps * layers / elapsed,
-                         "launches_timed": kern_n},
+                         "kernel_share_of_step": avg_launch_s * layers / (elapsed / steps),
+                         "launches_timed": kern_n,
+                         "timing": "separate pass (same l window): CUDA events around every "
+                                   "attend launch; the `value` pass records none"},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": launches,
             "gather": gather,
@@ -527,16 +680,24 @@ def main():
     ap.add_argument("--bits", type=int, default=0, choices=[0, 2, 4],
                     help="override the config's bit width (C4 sweeps 2 and 4)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--gather", action="store_true",
                     help="also time the optional NCCL all-gather of every layer's outputs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: batch per GPU (default); strong: fixed global batch (c4, c5)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU rehearsal of the rank/launch path (gloo, no GPU work)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    if args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
 

@@ -218,6 +218,10 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
 
 /* ---- measurement hooks (bench.py) --------------------------------------- */
 
+/* Re-reads the KIVI_* routing / tuning environment variables (read once per
+ * process otherwise; DESIGN.md §4 lists them).  Affects later calls only. */
+kivi_status kivi_reload_tuning(void);
+
 /* Selects the attend kernel: 0 = auto (fast sm_100a kernel when the shape is
  * supported, else generic), 1 = force generic, 2 = force fast (error if the
  * shape is unsupported). */

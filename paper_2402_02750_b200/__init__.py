@@ -20,7 +20,7 @@ __all__ = [
     "KiviError", "ShapeError", "UsageError", "ConfigError", "CudaError", "OutOfMemory",
     "CapacityError", "CacheConfig", "KVCache", "lib", "LIB_PATH", "HEADER_SYMBOLS",
     "quantize_matrix", "dequantize_matrix", "pack_codes", "unpack_codes",
-    "reference_attention",
+    "reference_attention", "reload_tuning",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -124,6 +124,7 @@ HEADER_SYMBOLS = {
     "kivi_pack_codes": (ctypes.c_int, [P, I64, I32, P, P]),
     "kivi_unpack_codes": (ctypes.c_int, [P, I64, I32, P, P]),
     "kivi_reference_attention": (ctypes.c_int, [P, I64, P, P, I64, I64, I32, P, P]),
+    "kivi_reload_tuning": (ctypes.c_int, []),
     "kivi_set_attend_path": (ctypes.c_int, [P, I32]),
     "kivi_profile_enable": (ctypes.c_int, [P, I32]),
     "kivi_profile_read": (ctypes.c_int, [P, P, P, P]),
@@ -161,17 +162,26 @@ def _torch():
     return torch
 
 
-def _stream_ptr(stream=None) -> int:
+def reload_tuning() -> None:
+    """Re-reads the KIVI_* routing knobs from the environment (kivi_reload_tuning)."""
+    _check(lib().kivi_reload_tuning())
+
+
+def _stream_ptr(stream=None, device=None) -> int:
+    """The given stream, else torch's current stream OF `device` (the cache's
+    device, which need not be the current one)."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
 
 
-def _dptr(t) -> int:
+def _dptr(t, device=None) -> int:
     if t is None:
         return None
     if not t.is_cuda:
         raise UsageError("expected a CUDA tensor")
+    if device is not None and t.device.index != device:
+        raise UsageError(f"tensor on cuda:{t.device.index}, cache on cuda:{device}")
     if not t.is_contiguous():
         raise UsageError("expected a contiguous tensor")
     return t.data_ptr()
@@ -244,11 +254,11 @@ class KVCache:
         return self.info()["total_tokens"]
 
     def reserve(self, capacity_tokens: int) -> None:
-        _check(lib().kivi_cache_reserve(self._h, int(capacity_tokens), _stream_ptr()))
+        _check(lib().kivi_cache_reserve(self._h, int(capacity_tokens), _stream_ptr(None, self.device)))
 
     def clone(self) -> "KVCache":
         h = ctypes.c_void_p()
-        _check(lib().kivi_cache_clone(self._h, _stream_ptr(), ctypes.byref(h)))
+        _check(lib().kivi_cache_clone(self._h, _stream_ptr(None, self.device), ctypes.byref(h)))
         return KVCache._wrap(self.cfg, self.n_units, self.device, h)
 
     def set_attend_path(self, path: str) -> None:
@@ -261,14 +271,14 @@ class KVCache:
         self._shape(values, 3, "prefill values")
         if keys.shape != values.shape:
             raise ShapeError("prefill: key/value token counts differ")
-        _check(lib().kivi_prefill(self._h, _dptr(keys), _dptr(values), int(keys.shape[1]),
-                                  _stream_ptr()))
+        _check(lib().kivi_prefill(self._h, _dptr(keys, self.device), _dptr(values, self.device), int(keys.shape[1]),
+                                  _stream_ptr(None, self.device)))
 
     def append(self, t_k, t_v) -> None:
         """t_k, t_v: [n_units, d] fp32 CUDA tensors."""
         self._rows(t_k, "append_token key")
         self._rows(t_v, "append_token value")
-        _check(lib().kivi_append(self._h, _dptr(t_k), _dptr(t_v), _stream_ptr()))
+        _check(lib().kivi_append(self._h, _dptr(t_k, self.device), _dptr(t_v, self.device), _stream_ptr(None, self.device)))
 
     def attend(self, q, q_per_kv: int = 1, weights: bool = False, scale_logits: bool = True,
                out=None):
@@ -282,8 +292,8 @@ class KVCache:
         if weights:
             w = torch.empty((self.n_units, q_per_kv, self.total_tokens), device=q.device,
                             dtype=torch.float32)
-        _check(lib().kivi_attend(self._h, _dptr(q.contiguous()), int(q_per_kv), _dptr(out),
-                                 _dptr(w), int(bool(scale_logits)), _stream_ptr()))
+        _check(lib().kivi_attend(self._h, _dptr(q.contiguous(), self.device), int(q_per_kv), _dptr(out, self.device),
+                                 _dptr(w, self.device), int(bool(scale_logits)), _stream_ptr(None, self.device)))
         return (out, w) if weights else out
 
     def decode(self, q, t_k, t_v, q_per_kv: int = 1, weights: bool = False,
@@ -304,9 +314,9 @@ class KVCache:
             raise ShapeError(f"query must be [n_units, q_per_kv, {d}] fp32")
         if out is None:
             out = torch.empty((U, q_per_kv, d), device=q.device, dtype=torch.float32)
-        _check(self._decode_fn(self._h, _dptr(q), _dptr(t_k), _dptr(t_v), int(q_per_kv),
-                               _dptr(out), None, int(bool(scale_logits)),
-                               torch.cuda.current_stream().cuda_stream))
+        _check(self._decode_fn(self._h, _dptr(q, self.device), _dptr(t_k, self.device), _dptr(t_v, self.device), int(q_per_kv),
+                               _dptr(out, self.device), None, int(bool(scale_logits)),
+                               torch.cuda.current_stream(self.device).cuda_stream))
         return out
 
     # ---- host-buffer path -------------------------------------------------
@@ -317,7 +327,7 @@ class KVCache:
         if k.shape != v.shape or k.ndim != 3:
             raise ShapeError("prefill: keys/values must both be [n_units, l, d]")
         _check(lib().kivi_prefill_host(self._h, k.ctypes.data, v.ctypes.data, k.shape[1],
-                                       _stream_ptr()))
+                                       _stream_ptr(None, self.device)))
 
     def decode_host(self, q, t_k, t_v, out, q_per_kv: int = 1, weights=None,
                     scale_logits: bool = True, stream=None) -> None:
@@ -327,11 +337,11 @@ class KVCache:
         _check(lib().kivi_decode_host(
             self._h, _hptr(q), _hptr(t_k), _hptr(t_v), int(q_per_kv), _hptr(out),
             _hptr(weights) if weights is not None else None, int(bool(scale_logits)),
-            _stream_ptr(stream)))
+            _stream_ptr(stream, self.device)))
 
     def host_join(self, stream=None) -> None:
         """Orders `stream` after every result copy decode_host has enqueued."""
-        _check(lib().kivi_host_join(self._h, _stream_ptr(stream)))
+        _check(lib().kivi_host_join(self._h, _stream_ptr(stream, self.device)))
 
     # ---- parity helpers -----------------------------------------------------
     def export_unit(self, unit: int) -> dict:
@@ -350,7 +360,7 @@ class KVCache:
             "value_residual": np.zeros((i["value_residual_rows"], d), np.float32),
         }
         st = _UnitState(*[b.ctypes.data if b.size else None for b in bufs.values()])
-        _check(lib().kivi_export_unit(self._h, int(unit), ctypes.byref(st), _stream_ptr()))
+        _check(lib().kivi_export_unit(self._h, int(unit), ctypes.byref(st), _stream_ptr(None, self.device)))
         return bufs
 
     def import_unit(self, unit: int, total_tokens: int, key_residual_capacity: int,
@@ -363,14 +373,14 @@ class KVCache:
         st = _UnitState(*[a.ctypes.data if a.size else None for a in arrs])
         _check(lib().kivi_import_unit(self._h, int(unit), int(total_tokens),
                                       int(key_residual_capacity), int(value_residual_capacity),
-                                      ctypes.byref(st), _stream_ptr()))
+                                      ctypes.byref(st), _stream_ptr(None, self.device)))
 
     def materialize(self):
         torch = _torch()
         l, d = self.total_tokens, self.cfg.head_dim
         k = torch.empty((self.n_units, l, d), device=f"cuda:{self.device}", dtype=torch.float32)
         v = torch.empty_like(k)
-        _check(lib().kivi_materialize(self._h, _dptr(k), _dptr(v), _stream_ptr()))
+        _check(lib().kivi_materialize(self._h, _dptr(k, self.device), _dptr(v, self.device), _stream_ptr(None, self.device)))
         return k, v
 
     # ---- measurement hooks ---------------------------------------------------
@@ -434,7 +444,7 @@ def quantize_matrix(m, bits: int, group_size: int, per_channel: bool):
     s = torch.zeros((max(ng, 1),), dtype=torch.float64, device=m.device)
     _check(lib().kivi_quantize_matrix(_dptr(m.contiguous()), rows, cols, bits, group_size,
                                       1 if per_channel else 0, _dptr(packed), _dptr(z),
-                                      _dptr(s), _stream_ptr()))
+                                      _dptr(s), _stream_ptr(None, m.device)))
     return packed, z[:ng], s[:ng]
 
 
@@ -443,7 +453,7 @@ def dequantize_matrix(packed, zero, scale, rows, cols, bits, group_size, per_cha
     out = torch.empty((rows, cols), dtype=torch.float32, device=packed.device)
     _check(lib().kivi_dequantize_matrix(_dptr(packed), _dptr(zero), _dptr(scale), rows, cols,
                                         bits, group_size, 1 if per_channel else 0, _dptr(out),
-                                        _stream_ptr()))
+                                        _stream_ptr(None, packed.device)))
     return out
 
 
@@ -451,14 +461,14 @@ def pack_codes(codes, bits: int):
     torch = _torch()
     n = codes.numel()
     out = torch.zeros(((n * bits + 7) // 8,), dtype=torch.uint8, device=codes.device)
-    _check(lib().kivi_pack_codes(_dptr(codes), n, bits, _dptr(out), _stream_ptr()))
+    _check(lib().kivi_pack_codes(_dptr(codes), n, bits, _dptr(out), _stream_ptr(None, codes.device)))
     return out
 
 
 def unpack_codes(packed, n: int, bits: int):
     torch = _torch()
     out = torch.zeros((n,), dtype=torch.uint8, device=packed.device)
-    _check(lib().kivi_unpack_codes(_dptr(packed), n, bits, _dptr(out), _stream_ptr()))
+    _check(lib().kivi_unpack_codes(_dptr(packed), n, bits, _dptr(out), _stream_ptr(None, packed.device)))
     return out
 
 
@@ -470,5 +480,5 @@ def reference_attention(q, K, V, scale_logits: bool = True):
     out = torch.empty((nq, d), dtype=torch.float32, device=q.device)
     _check(lib().kivi_reference_attention(_dptr(q.contiguous()), nq, _dptr(K.contiguous()),
                                           _dptr(V.contiguous()), l, d, int(bool(scale_logits)),
-                                          _dptr(out), _stream_ptr()))
+                                          _dptr(out), _stream_ptr(None, q.device)))
     return out

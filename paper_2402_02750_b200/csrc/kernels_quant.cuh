@@ -183,7 +183,70 @@ __device__ __forceinline__ void minmax_pair_reduce8(float& lo, int& ilo, float& 
 // One unit's append_token by one warp (d = 128, G = 32).  Also called by the
 // residual-window attend kernel, which appends each unit it owns right before
 // streaming that unit's residual items (kivi_decode's fused route).
+// One token row (d = 128) quantized per-token into d/32 groups by a warp:
+// lane j holds channels 4j..4j+3 (x); writes the row's d*B/32 code words and
+// its 4 (lo, hi) pairs.  Ties in the group min / max follow
+// std::minmax_element (first smallest, last largest) via the channel index.
 template <int B>
+__device__ __forceinline__ void value_row_fast(const float4 v, int lane, uint32_t* __restrict__ vw,
+                                               float2* __restrict__ vp) {
+    const float x[4] = {v.x, v.y, v.z, v.w};
+    float lo = x[0], hi = x[0];
+    int ilo = 4 * lane, ihi = 4 * lane;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+        if (x[i] < lo) { lo = x[i]; ilo = 4 * lane + i; }
+        if (!(x[i] < hi)) { hi = x[i]; ihi = 4 * lane + i; }
+    }
+    minmax_pair_reduce8(lo, ilo, hi, ihi);
+    const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bits |= quant_code(cc, x[i]) << (B * i);
+    // lane's 4 codes -> position (4*lane*B) of the token's 128*B-bit row
+    uint32_t word = bits << ((4 * lane * B) & 31);
+    constexpr int LPW = 32 / (4 * B);  // lanes sharing one 32-bit word
+#pragma unroll
+    for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+    if ((lane % LPW) == 0) vw[(4 * lane * B) >> 5] = word;
+    if ((lane & 7) == 0) vp[lane >> 3] = make_float2(lo, hi);
+}
+
+// One per-channel key group (32 tokens of one channel, in token order) ->
+// its B code words (token i at bits B*(i % (32/B)) of word i / (32/B)) and
+// (lo, hi); sequential over the tokens, so first-min / last-max are exact.
+template <int B>
+__device__ __forceinline__ float2 key_group_fast(const float (&x)[32], uint32_t (&w)[B]) {
+    float lo = x[0], hi = x[0];
+#pragma unroll
+    for (int i = 1; i < 32; ++i) minmax_step(x[i], lo, hi);
+    const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+    constexpr int CPW = 32 / B;  // codes per word
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) word |= quant_code(cc, x[k * CPW + i]) << (B * i);
+        w[k] = word;
+    }
+    return make_float2(lo, hi);
+}
+
+template <int B>
+__device__ __forceinline__ void store_key_words(uint32_t* dst, const uint32_t (&w)[B]) {
+    if constexpr (B == 2) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+    } else if constexpr (B == 4) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < B; ++k) dst[k] = w[k];
+    }
+}
+
+// FLUSH = false leaves the key flush to the flush warps of
+// append_flush_fast_kernel (the serial per-warp flush below takes ~130 us).
+template <int B, bool FLUSH = true>
 __device__ __forceinline__ void append_unit_fast(const CacheDev& c, const float* __restrict__ tk,
                                                  const float* __restrict__ tv, int64_t l,
                                                  int64_t u, int lane) {
@@ -200,31 +263,13 @@ __device__ __forceinline__ void append_unit_fast(const CacheDev& c, const float*
         // value FIFO pop: quantize the oldest row (token l - R) per-token
         const int64_t e = l - R;
         const float4 old = reinterpret_cast<const float4*>(vring + (int64_t)slot * D)[lane];
-        const float x[4] = {old.x, old.y, old.z, old.w};
-        float lo = x[0], hi = x[0];
-        int ilo = 4 * lane, ihi = 4 * lane;
-#pragma unroll
-        for (int i = 1; i < 4; ++i) {
-            if (x[i] < lo) { lo = x[i]; ilo = 4 * lane + i; }
-            if (!(x[i] < hi)) { hi = x[i]; ihi = 4 * lane + i; }
-        }
-        minmax_pair_reduce8(lo, ilo, hi, ihi);
-        const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
-        uint32_t bits = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) bits |= quant_code(cc, x[i]) << (B * i);
-        // lane's 4 codes -> position (4*lane*B) of the token's 128*B-bit row
-        uint32_t word = bits << ((4 * lane * B) & 31);
-        constexpr int LPW = 32 / (4 * B);  // lanes sharing one 32-bit word
-#pragma unroll
-        for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
-        uint32_t* vw = reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + e * (D * B / 32);
-        if ((lane % LPW) == 0) vw[(4 * lane * B) >> 5] = word;
-        if ((lane & 7) == 0) c.vpairs[u * c.vp_ustride + e * (D / G) + (lane >> 3)] = make_float2(lo, hi);
+        value_row_fast<B>(old, lane,
+                          reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + e * (D * B / 32),
+                          c.vpairs + u * c.vp_ustride + e * (D / G));
     }
     reinterpret_cast<float4*>(vring + (int64_t)slot * D)[lane] = vv;
 
-    if ((l + 1) % R == 0) {
+    if (FLUSH && (l + 1) % R == 0) {
         // key flush: quantize the R x 128 ring per-channel into R/32 tiles;
         // lane owns channels lane, lane+32, lane+64, lane+96 (sequential over
         // the 32 tokens of a group: exact first-min / last-max order).
@@ -261,7 +306,94 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
     const int lane = threadIdx.x & 31;
     const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (u >= c.n_units) return;
-    append_unit_fast<B>(c, tk, tv, l, u, lane);
+    append_unit_fast<B, false>(c, tk, tv, l, u, lane);
+}
+
+// The append of a flush step ((l + 1) % R == 0): blocks [0, n_app) append one
+// unit per warp (no flush); the remaining blocks flush the key ring, one
+// thread per (unit, 32-token tile, channel) group: lanes are 32 consecutive
+// channels, so every token row is one coalesced 128-byte load per warp and the
+// group's code words one contiguous store.  The ring's last row (token l) is
+// read from t_k, which the append warps write concurrently.
+template <int B>
+__global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
+                                                                const float* __restrict__ tk,
+                                                                const float* __restrict__ tv,
+                                                                int64_t l, int n_app) {
+    pdl_trigger();
+    constexpr int D = 128, G = 32;
+    const int lane = threadIdx.x & 31;
+    if ((int)blockIdx.x < n_app) {
+        const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (u < c.n_units) append_unit_fast<B, false>(c, tk, tv, l, u, lane);
+        return;
+    }
+    const int tiles = c.R / G;
+    const int64_t fw = (int64_t)(blockIdx.x - n_app) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t u = fw / (tiles * (D / 32));
+    if (u >= c.n_units) return;
+    const int rem = (int)(fw % (tiles * (D / 32)));
+    const int tl = rem / (D / 32);
+    const int ch = (rem % (D / 32)) * 32 + lane;
+    const float* kring = c.kring + u * c.ring_ustride;
+    const int last = c.R - 1;  // ring row of token l (written by this launch)
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int r = tl * G + i;
+        x[i] = r == last ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
+    }
+    uint32_t w[B];
+    const float2 lh = key_group_fast<B>(x, w);
+    const int64_t g = ((l + 1 - c.R) / G + tl) * D + ch;
+    store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
+    c.kpairs[u * c.kp_ustride + g] = lh;
+}
+
+// ---- bulk prefill for d = 128, G = 32, B in {2, 4} --------------------------
+// Keys: one thread per (unit, tile, channel) group, lanes on consecutive
+// channels (coalesced token rows), whole code words stored (no atomics).
+template <int B>
+__global__ void __launch_bounds__(256) prefill_keys_fast_kernel(CacheDev c,
+                                                                const float* __restrict__ keys,
+                                                                int64_t l, int64_t kg) {
+    constexpr int D = 128, G = 32;
+    const int64_t per_unit = (kg / G) * D;
+    const int64_t total = per_unit * c.n_units;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        const int64_t g = gid % per_unit;  // tg * D + ch
+        const int64_t tg = g / D, ch = g % D;
+        const float* src = keys + (u * l + tg * G) * D + ch;
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __ldcs(src + (int64_t)i * D);
+        uint32_t w[B];
+        const float2 lh = key_group_fast<B>(x, w);
+        store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
+        c.kpairs[u * c.kp_ustride + g] = lh;
+    }
+}
+
+// Values: one warp per token row (512 B, one float4 per lane), the row's four
+// 32-channel groups reduced across 8 lanes each (value_row_fast).
+template <int B>
+__global__ void __launch_bounds__(256) prefill_values_fast_kernel(CacheDev c,
+                                                                  const float* __restrict__ values,
+                                                                  int64_t l, int64_t vg) {
+    constexpr int D = 128, G = 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = vg * c.n_units;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+         r += nw) {
+        const int64_t u = r / vg, t = r % vg;
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(values + (u * l + t) * D) + lane);
+        value_row_fast<B>(v, lane,
+                          reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + t * (D * B / 32),
+                          c.vpairs + u * c.vp_ustride + t * (D / G));
+    }
 }
 
 // ---- materialize (reference materialize_*, kv_cache.cpp:100-106) ---------
@@ -325,10 +457,13 @@ __global__ void zs_to_pairs_kernel(const double* __restrict__ z, const double* _
          i += (int64_t)gridDim.x * blockDim.x) {
         float lo = (float)z[i];
         float hi = (float)__dadd_rn(z[i], __dmul_rn(s[i], (double)maxc));
-        if (s[i] == 1.0 && hi != lo) {
-            // Degenerate groups (s == 1, all codes 0) and genuine s == 1 groups
-            // both dequantise to z + code; keep hi as computed.
-        }
+        // A degenerate group (reference hi == lo: scale 1.0, every code 0) must
+        // export scale 1.0 again.  float(z + maxc) need not land exactly maxc
+        // above z (z = 0.1f, B = 2 re-exports 0.99999997), so such a group is
+        // stored as hi == lo.  A genuine scale-1.0 group has hi - lo == maxc up
+        // to double rounding and round-trips through the first branch; its
+        // dequantisation is unchanged either way (codes 0 give z).
+        if (s[i] == 1.0 && group_scale(lo, hi, maxc) != 1.0) hi = lo;
         pairs[i] = make_float2(lo, hi);
     }
 }

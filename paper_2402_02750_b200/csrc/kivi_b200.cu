@@ -87,9 +87,15 @@ struct Scratch {
         if (p) cudaFree(p);
     }
 };
+// One set per (host thread, device): a thread that drives several GPUs gets
+// separate buffers on each.
+constexpr int kMaxDevices = 64;
 Scratch& scratch(int slot) {
-    thread_local Scratch s[4];
-    return s[slot];
+    thread_local Scratch s[kMaxDevices][4];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    return s[dev][slot];
 }
 
 }  // namespace
@@ -309,15 +315,55 @@ int env_int(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 
-int g_num_sms = 0;
-int num_sms() {
-    if (!g_num_sms) {
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+// Routing / tuning knobs, read from the environment once per process and
+// again on kivi_reload_tuning() (tests flip them between cases).  Defaults are
+// the measured-best settings.
+struct Tuning {
+    int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
+    int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
+    int gqa_tc, gqa_partial, gqa_tail_ctas;
+    void load() {
+        fused_append = env_int("KIVI_FUSED_APPEND", 0);
+        tail_side = env_int("KIVI_TAIL_SIDE", 1);
+        small_items = env_int("KIVI_SMALL_ITEMS", 1);
+        small_fused = env_int("KIVI_SMALL_FUSED", 0);
+        small_sub = env_int("KIVI_SMALL_SUB", 0);
+        combine_parallel = env_int("KIVI_COMBINE_PARALLEL", 1);
+        tail_sub = env_int("KIVI_TAIL_SUB", 256);
+        res_sub = env_int("KIVI_RES_SUB", 32);
+        res_sub_body = env_int("KIVI_RES_SUB_BODY", 0);
+        mha_tc = env_int("KIVI_MHA_TC", 0);
+        pdl = env_int("KIVI_PDL", 1);
+        tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
+        tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
+        tail_last = env_int("KIVI_TAIL_LAST", 0);
+        gqa_tc = env_int("KIVI_GQA_TC", 1);
+        gqa_partial = env_int("KIVI_GQA_PARTIAL", 1);
+        gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
     }
-    return g_num_sms;
+};
+Tuning g_tune;
+bool g_tune_loaded = false;
+const Tuning& tune() {
+    if (!g_tune_loaded) {
+        g_tune.load();
+        g_tune_loaded = true;
+    }
+    return g_tune;
+}
+
+int g_num_sms[kMaxDevices] = {};
+// SM count of the current device (callers hold a DeviceGuard for the cache).
+int num_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (!g_num_sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = n > 0 ? n : 148;
+    }
+    return g_num_sms[dev];
 }
 
 // Whether kivi_decode may fold this step's append into the residual-window
@@ -326,15 +372,15 @@ int num_sms() {
 bool fused_append_ok(const kivi_cache* h, int q_per_kv) {
     // off by default: measured C2 8.73 vs 8.49 ms/step (the append lengthens the
     // residual items, which sit on the critical path); read per call (tests flip it)
-    const int on = env_int("KIVI_FUSED_APPEND", 0);
-    static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
+    const int on = tune().fused_append;
+    const int tail_side = tune().tail_side;
     const kivi_config& c = h->cfg;
     if (!on || !tail_side || q_per_kv != 1 || h->attend_path == 1) return false;
     if (c.head_dim != 128 || c.group_size != 32 || (c.bits != 2 && c.bits != 4)) return false;
     const int64_t l = h->l + 1, R = c.residual_length;
     const int64_t vg = l - std::min(l, R);
     const bool latency_bound =
-        env_int("KIVI_SMALL_ITEMS", 1) && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
+        tune().small_items && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
     return !latency_bound && vg > 0 && ((vg - 1) / 32 * 32) / fast::BSUB > 0;
 }
 
@@ -344,10 +390,10 @@ bool small_fused_ok(const kivi_cache* h, int q_per_kv) {
     const kivi_config& c = h->cfg;
     // off by default: measured slower on C1 (51.6 vs 22.1 + append + combine us):
     // the grid barrier and the last-warp merges serialise latency-bound phases
-    if (!env_int("KIVI_SMALL_FUSED", 0) || q_per_kv != 1 || h->attend_path == 1) return false;
+    if (!tune().small_fused || q_per_kv != 1 || h->attend_path == 1) return false;
     if (c.head_dim != 128 || c.group_size != 32 || (c.bits != 2 && c.bits != 4)) return false;
     const int64_t l = h->l + 1;
-    return env_int("KIVI_SMALL_ITEMS", 1) && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
+    return tune().small_items && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms();
 }
 
 template <int B>
@@ -355,7 +401,7 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
                                float* out, float* weights, float qscale, int64_t l_app,
                                cudaStream_t st) {
     const int64_t U = h->n_units;
-    static const int tsub = std::max(32, std::min(fast::SUB, env_int("KIVI_SMALL_SUB", 64)) / 32 * 32);
+    const int tsub = std::max(32, std::min(fast::SUB, tune().small_sub > 0 ? tune().small_sub : 64) / 32 * 32);
     const int64_t n_sub = ceil_div(h->l, tsub);
     if (h->l >= (1LL << 30) || U * n_sub >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "fast attend path: cache too large for 32-bit indexing");
@@ -371,7 +417,8 @@ kivi_status launch_small_fused(kivi_cache* h, const float* q, const float* tk, c
         KIVI_CUDA(cudaMemsetAsync(h->small_sync, 0, sizeof(unsigned long long) * (1 + U), st));
     }
     const int smem = fast::WS2::STRIDE * fast::WARPS;
-    static int per_sm = 0;
+    // per cache (so per device): the attribute must be set on each device
+    int& per_sm = h->fast_per_sm[B][3];
     if (!per_sm) {
         KIVI_CUDA(cudaFuncSetAttribute(fast::attend_tail_kernel<B, fast::WARPS, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -452,7 +499,7 @@ static void take_work_slot(kivi_cache* h, fast::FastArgs& a) {
 // C3 17.7 vs 21.8, C5 13.2 vs 20.7 us per layer); KIVI_COMBINE_PARALLEL=0
 // selects the serial per-channel merge.
 static int combine_parallel(int64_t rows) {
-    static const int force = env_int("KIVI_COMBINE_PARALLEL", 1);
+    const int force = tune().combine_parallel;
     (void)rows;
     return force ? 1 : 0;
 }
@@ -483,12 +530,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // Items: body = whole BSUB-token sub-chunks below floor32(vg) (all keys and
     // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
     // hold the fp32 residual rows.  One partial slot per item.
-    static const int tsub_env = std::max(32, std::min(fast::SUB, env_int("KIVI_TAIL_SUB", 256)) / 32 * 32);
+    const int tsub_env = std::max(32, std::min(fast::SUB, tune().tail_sub) / 32 * 32);
     // few-unit route item size: KIVI_SMALL_SUB, or (0, default) sized so the
     // items below the residual window about fill the resident warps once
     // (C1: 32 units x 3968 tokens / 1776 warps -> 96 tokens; 64 measured
     // 18.3 us, 96 16.2 us, 128 18.0 us)
-    static const int tsub_small_env = env_int("KIVI_SMALL_SUB", 0);
+    const int tsub_small_env = tune().small_sub;
     static const int tsub_small_min = 32;
     const int64_t res_warps = (int64_t)num_sms() * 3 * fast::WARPS;  // tail kernel: 3 CTAs / SM
     const int tsub_small =
@@ -501,7 +548,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // Few units (e.g. one sequence's 32 heads): 256-token body items leave
     // most warps idle and the per-unit residual item becomes the critical
     // path, so every token goes through tsub-token items instead.
-    const int small_items = env_int("KIVI_SMALL_ITEMS", 1);  // read per call (tests flip it)
+    const int small_items = tune().small_items;
     const bool latency_bound = small_items && U * ceil_div(h->l, fast::BSUB) < 4 * num_sms();
     // fused append: the body must not cover the token the append pops into the
     // quantized store (token vg - 1), so it stops at floor32(vg - 1)
@@ -512,10 +559,10 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int64_t t_first = nfull * fast::BSUB;
     const int tsub = latency_bound ? tsub_small : tsub_env;
     // few-unit route: the residual window [floor32(vg), l) in rsub-token items
-    static const int rsub_env = env_int("KIVI_RES_SUB", 32) / 32 * 32;
+    const int rsub_env = tune().res_sub / 32 * 32;
     // (KIVI_RES_SUB_BODY=1: on the body route too; measured slower on C2,
     // within noise on C5)
-    static const bool rsub_body = env_int("KIVI_RES_SUB_BODY", 0) != 0;
+    const bool rsub_body = tune().res_sub_body != 0;
     const int rsub = ((latency_bound || rsub_body) && l_app < 0 && rsub_env > 0) ? rsub_env : 0;
     const int64_t t_b = rsub ? (h->vg() / 32) * 32 : h->l;
     const int64_t n_a = ceil_div(t_b - t_first, tsub);
@@ -551,7 +598,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int smem = fast::WS2::STRIDE * fast::WARPS;
     const int smem_body = fast::WSB::STRIDE * fast::WARPS;
     const int smem_tc = gqa_tc::TS<1>::STRIDE * gqa_tc::WARPS;
-    static const int mha_tc = env_int("KIVI_MHA_TC", 0);  // measured slower on C2
+    const int mha_tc = tune().mha_tc;  // measured slower on C2
     if (h->fast_per_sm[B][0] == 0) {
         KIVI_CUDA(cudaFuncSetAttribute(gqa_tc::attend_gqa_tc_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
@@ -591,10 +638,10 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int) * WORK_SLOTS, st));
     }
     const bool has_tail = n_sub > nfull;
-    static const int use_pdl = env_int("KIVI_PDL", 1);
-    static const int tail_side = env_int("KIVI_TAIL_SIDE", 1);
-    static const int tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
-    static const int tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
+    const int use_pdl = tune().pdl;
+    const int tail_side = tune().tail_side;
+    const int tail_ctas = tune().tail_ctas;
+    const int tail_warp_ctas = tune().tail_warp_ctas;
     // Body and tail concurrently.  Default: one stream, programmatic launches
     // (append -> tail -> body -> combine): the tail waits for the append, then
     // triggers, so the body's CTAs start beside it (the body reads only what
@@ -604,7 +651,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const bool one_stream = use_pdl && nfull > 0 && has_tail && l_app < 0 && !tail_warp_ctas &&
                             !(B == 2 && mha_tc);
     cudaStream_t tail_st = (tail_side && nfull > 0 && !one_stream) ? h->side : st;
-    static const int tail_last_env = env_int("KIVI_TAIL_LAST", 0);
+    const int tail_last_env = tune().tail_last;
     const bool tail_last = one_stream && tail_last_env;
     fast::FastArgs a_tail{};
     bool tail_deferred = false;
@@ -667,7 +714,9 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.n_items = (int)(U * nfull);
         take_work_slot(h, a);
         if (B == 2 && mha_tc && fast::BSUB == fast::SUB) {
-            // tensor-core body (kernels_attend_gqa_tc.cuh with one query head)
+            // tensor-core body (kernels_attend_gqa_tc.cuh with one query head):
+            // every item is a whole SUB-token sub-chunk below nfull * BSUB
+            a.body_end = (int)(nfull * fast::BSUB);
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][2],
                                                    ceil_div(a.n_items, gqa_tc::WARPS));
             gqa_tc::attend_gqa_tc_kernel<1>
@@ -733,10 +782,10 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     if (h->l >= (1LL << 30) || U * ceil_div(h->l, fast::SUB) >= (1LL << 30))
         return fail(KIVI_ERR_CONFIG, "GQA attend path: cache too large for 32-bit indexing");
     const int64_t n_sub = ceil_div(h->l, fast::SUB);
-    static const int use_tc = env_int("KIVI_GQA_TC", 1);
+    const int use_tc = tune().gqa_tc;
     // body = [0, floor32(vg)) (partial last item): the CUDA-core residual items
     // then hold fewer than 32 quantized values
-    static const int partial = env_int("KIVI_GQA_PARTIAL", 1);
+    const int partial = tune().gqa_partial;
     const int64_t body_end =
         use_tc ? (partial ? (h->vg() / 32) * 32 : (h->vg() / 32 * 32) / fast::SUB * fast::SUB) : 0;
     const int64_t nfull = ceil_div(body_end, fast::SUB);
@@ -793,7 +842,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         KIVI_CUDA(cudaMemsetAsync(h->work, 0, sizeof(int) * WORK_SLOTS, st));
     }
     const bool has_tail = ntail > 0;
-    static const int tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
+    const int tail_ctas = tune().gqa_tail_ctas;
     cudaStream_t tail_st = nfull > 0 ? h->side : st;
     if (has_tail) {
         // items holding fp32 residual rows: CUDA-core kernel, concurrently
@@ -930,7 +979,11 @@ kivi_status kivi_cache_create(const kivi_config* cfg, int device, int64_t n_unit
 kivi_status kivi_cache_destroy(kivi_cache* h) {
     if (!h) return KIVI_OK;
     DeviceGuard g(h->device);
-    cudaDeviceSynchronize();
+    // the caller's streams must be done with the cache (as for any free); the
+    // cache's own copy / side streams are drained here, not the whole device
+    if (h->side) cudaStreamSynchronize(h->side);
+    if (h->h2d) cudaStreamSynchronize(h->h2d);
+    if (h->d2h) cudaStreamSynchronize(h->d2h);
     free_cache_buffers(h);
     cudaFree(h->part_o);
     cudaFree(h->part_ml);
@@ -1087,13 +1140,24 @@ kivi_status kivi_prefill(kivi_cache* h, const float* keys, const float* values, 
     const int64_t kg = l - l % R;
     const int64_t vg = l - std::min(l, R);
     const int64_t G = h->cfg.group_size, d = h->cfg.head_dim;
+    const bool fast = d == 128 && G == 32 && (c.bits == 2 || c.bits == 4);
     if (kg > 0) {
-        prefill_keys_kernel<<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
+        if (fast && c.bits == 2)
+            prefill_keys_fast_kernel<2><<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
+        else if (fast)
+            prefill_keys_fast_kernel<4><<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
+        else
+            prefill_keys_kernel<<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
     if (vg > 0) {
-        prefill_values_kernel<<<grid_for(U * vg * (d / G)), 256, 0, st>>>(c, values, l, vg);
+        if (fast && c.bits == 2)
+            prefill_values_fast_kernel<2><<<grid_for(U * vg * 32), 256, 0, st>>>(c, values, l, vg);
+        else if (fast)
+            prefill_values_fast_kernel<4><<<grid_for(U * vg * 32), 256, 0, st>>>(c, values, l, vg);
+        else
+            prefill_values_kernel<<<grid_for(U * vg * (d / G)), 256, 0, st>>>(c, values, l, vg);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
@@ -1123,10 +1187,21 @@ static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t
     const kivi_config& cf = h->cfg;
     if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4)) {
         const unsigned grid = (unsigned)ceil_div(h->n_units, 8);
-        if (cf.bits == 2)
+        if ((h->l + 1) % cf.residual_length == 0) {
+            // key flush step: extra blocks quantize the ring, one thread per group
+            const int64_t groups = h->n_units * (cf.residual_length / 32) * 128;
+            const unsigned fgrid = (unsigned)ceil_div(groups, 256);
+            if (cf.bits == 2)
+                append_flush_fast_kernel<2><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
+                                                                         (int)grid);
+            else
+                append_flush_fast_kernel<4><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
+                                                                         (int)grid);
+        } else if (cf.bits == 2) {
             append_fast_kernel<2><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
-        else
+        } else {
             append_fast_kernel<4><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
+        }
     } else {
         append_kernel<<<(unsigned)h->n_units, 128, 0, st>>>(h->dev, t_k, t_v, h->l);
     }
@@ -1616,6 +1691,12 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
     cudaError_t se = cudaStreamSynchronize(st);
     if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(le));
     if (se != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(se));
+    return KIVI_OK;
+}
+
+kivi_status kivi_reload_tuning(void) {
+    g_tune.load();
+    g_tune_loaded = true;
     return KIVI_OK;
 }
 

@@ -19,6 +19,38 @@ os.environ.setdefault("KIVI_SMALL_ITEMS", "0")
 os.environ.setdefault("KIVI_SMALL_FUSED", "0")
 
 
+def _reload_tuning():
+    try:
+        import paper_2402_02750_b200 as kb
+        if os.path.exists(kb.LIB_PATH):
+            kb.reload_tuning()
+    except Exception:
+        pass
+
+
+@pytest.fixture(autouse=True)
+def _kivi_tuning(monkeypatch):
+    """The library reads its KIVI_* routing knobs once (kivi_reload_tuning
+    re-reads them): reload at the start of every test (the previous test's
+    monkeypatch has been undone) and on every monkeypatched KIVI_* change."""
+    _reload_tuning()
+    orig_set, orig_del = monkeypatch.setenv, monkeypatch.delenv
+
+    def setenv(name, value, prepend=None):
+        orig_set(name, value, prepend)
+        if name.startswith("KIVI_"):
+            _reload_tuning()
+
+    def delenv(name, raising=True):
+        orig_del(name, raising)
+        if name.startswith("KIVI_"):
+            _reload_tuning()
+
+    monkeypatch.setenv = setenv
+    monkeypatch.delenv = delenv
+    yield
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
 

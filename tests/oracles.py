@@ -370,6 +370,14 @@ class RefUnit:
         K, V = np.ascontiguousarray(K, np.float32), np.ascontiguousarray(V, np.float32)
         self.ref._chk(self.L.ref_prefill(self.h, *self.cfg, _p(K), _p(V), K.shape[0]))
 
+    def clone(self):
+        """Deep copy of the state (the reference's states are copyable,
+        workload.cpp:166-167): one prefill serves several query heads."""
+        c = RefUnit.__new__(RefUnit)
+        c.ref, c.L, c.cfg, c.d = self.ref, self.L, self.cfg, self.d
+        c.h = self.L.ref_state_clone(self.h)
+        return c
+
     def append(self, tk, tv):
         tk, tv = np.ascontiguousarray(tk, np.float32), np.ascontiguousarray(tv, np.float32)
         self.ref._chk(self.L.ref_append(self.h, *self.cfg, _p(tk), _p(tv)))
