@@ -164,6 +164,53 @@ kivi_status kivi_decode_host(kivi_cache* cache, const float* t_q, const float* t
 /* Orders `stream` after every result copy kivi_decode_host has enqueued. */
 kivi_status kivi_host_join(kivi_cache* cache, void* stream);
 
+/* ---- one decode step of a whole model ------------------------------------
+ * caches[i] holds layer i (all with the same n_units, head_dim and device);
+ * the reference's decode loop runs the layers of a step in order
+ * (workload.cpp:224-242).  Row layouts, layer-major:
+ *   t_q, out: [n_layers][n_units][q_per_kv][d];  t_k, t_v: [n_layers][n_units][d].
+ * kivi_decode_layers: device pointers, enqueued on `stream`, no sync.
+ * kivi_decode_layers_host: host pointers (pinned for speed); uploads every
+ * layer's rows, decodes every layer and copies the outputs back, then
+ * synchronises `stream`: the outputs are on the host when it returns.  With
+ * KIVI_STEP_GRAPH=1 (and a non-NULL stream) the step is captured as a CUDA
+ * graph and replayed (cudaGraphExecUpdate between steps). */
+kivi_status kivi_decode_layers(kivi_cache* const* caches, int32_t n_layers, const float* t_q,
+                               const float* t_k, const float* t_v, int32_t q_per_kv, float* out,
+                               int32_t scale_logits, void* stream);
+kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers, const float* t_q,
+                                    const float* t_k, const float* t_v, int32_t q_per_kv,
+                                    float* out, int32_t scale_logits, void* stream);
+
+/* ---- q/k/v projection fused with the append ------------
+ * The reference projects each decode token per layer, q = t W_q, k = t W_k,
+ * v = t W_v in fp32 (workload.cpp:230-232).  kivi_proj holds one layer's
+ * three [hidden_in][hidden_out] weight matrices (x @ W convention, device
+ * pointers, copied and transposed once); the GEMM runs on the tcgen05 tensor
+ * cores in 3xTF32 (fp32-class accuracy).
+ * kivi_proj_gemm: x [n][hidden_in] -> out_q/k/v; seq == 0: [n][hidden_out];
+ *   seq > 0: rows are (sequence, token) = (r / seq, r % seq) and the outputs
+ *   are written per unit, [n / seq * heads][seq][128] (kivi_prefill's layout).
+ * kivi_proj_append: the decode step's projection + append in one launch:
+ *   q -> q_out [n * heads][128]; k and v are appended to `cache` (n_units =
+ *   n * heads, head_dim 128, group 32, 2 or 4 bits) as kivi_append would,
+ *   with the value FIFO pop quantized in the GEMM epilogue.  Follow with
+ *   kivi_attend (together: the reference decode_attention). */
+typedef struct kivi_proj kivi_proj;
+kivi_status kivi_proj_create(int device, int64_t hidden_in, int64_t hidden_out, const float* w_q,
+                             const float* w_k, const float* w_v, void* stream, kivi_proj** out);
+kivi_status kivi_proj_destroy(kivi_proj* proj);
+kivi_status kivi_proj_gemm(kivi_proj* proj, const float* x, int64_t n, float* out_q, float* out_k,
+                           float* out_v, int64_t seq, void* stream);
+kivi_status kivi_proj_append(kivi_proj* proj, kivi_cache* cache, const float* x, int64_t n,
+                             float* q_out, void* stream);
+
+/* Step-graph counters of the calling thread on the current device: steps
+ * replayed as a graph, graph re-instantiations (topology changed), captures
+ * that failed (run directly instead). */
+kivi_status kivi_step_graph_stats(int64_t* replayed, int64_t* reinstantiated,
+                                  int64_t* capture_failed);
+
 /* ---- state exchange in the reference layout (parity / drop-in facade) ---- */
 
 /* Copies unit `unit` to host buffers; synchronises `stream`. */

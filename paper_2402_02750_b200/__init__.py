@@ -20,7 +20,7 @@ __all__ = [
     "KiviError", "ShapeError", "UsageError", "ConfigError", "CudaError", "OutOfMemory",
     "CapacityError", "CacheConfig", "KVCache", "lib", "LIB_PATH", "HEADER_SYMBOLS",
     "quantize_matrix", "dequantize_matrix", "pack_codes", "unpack_codes",
-    "reference_attention", "reload_tuning",
+    "reference_attention", "reload_tuning", "LayerStack", "Projection",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -114,6 +114,13 @@ HEADER_SYMBOLS = {
     "kivi_append_host": (ctypes.c_int, [P, P, P, P]),
     "kivi_decode_host": (ctypes.c_int, [P, P, P, P, I32, P, P, I32, P]),
     "kivi_host_join": (ctypes.c_int, [P, P]),
+    "kivi_decode_layers": (ctypes.c_int, [P, I32, P, P, P, I32, P, I32, P]),
+    "kivi_decode_layers_host": (ctypes.c_int, [P, I32, P, P, P, I32, P, I32, P]),
+    "kivi_step_graph_stats": (ctypes.c_int, [P, P, P]),
+    "kivi_proj_create": (ctypes.c_int, [ctypes.c_int, I64, I64, P, P, P, P, P]),
+    "kivi_proj_destroy": (ctypes.c_int, [P]),
+    "kivi_proj_gemm": (ctypes.c_int, [P, P, I64, P, P, P, I64, P]),
+    "kivi_proj_append": (ctypes.c_int, [P, P, P, I64, P, P]),
     "kivi_export_unit": (ctypes.c_int, [P, I64, P, P]),
     "kivi_import_unit": (ctypes.c_int, [P, I64, I64, I64, I64, P, P]),
     "kivi_materialize": (ctypes.c_int, [P, P, P, P]),
@@ -416,6 +423,99 @@ class KVCache:
         torch = _torch()
         if t.numel() != self.n_units * self.cfg.head_dim or t.dtype != torch.float32:
             raise ShapeError(f"{what}: expected 1x{self.cfg.head_dim} rows per unit")
+
+
+class LayerStack:
+    """The caches of a model's layers (same units / head_dim / device), decoded
+    one whole step per C-ABI call (kivi_decode_layers[_host]): the host loop
+    over layers runs in native code."""
+
+    def __init__(self, caches):
+        self.caches = list(caches)
+        if not self.caches:
+            raise UsageError("LayerStack: no caches")
+        self.device = self.caches[0].device
+        self._arr = (ctypes.c_void_p * len(self.caches))(*[c._h.value for c in self.caches])
+
+    def decode(self, q, t_k, t_v, out, q_per_kv: int = 1, scale_logits: bool = True) -> None:
+        """Device tensors: q/out [L, U, q_per_kv, d], t_k/t_v [L, U, d]."""
+        dv = self.device
+        _check(lib().kivi_decode_layers(self._arr, len(self.caches), _dptr(q, dv), _dptr(t_k, dv),
+                                        _dptr(t_v, dv), int(q_per_kv), _dptr(out, dv),
+                                        int(bool(scale_logits)), _stream_ptr(None, dv)))
+
+    def decode_host(self, q, t_k, t_v, out, q_per_kv: int = 1, scale_logits: bool = True,
+                    stream=None) -> None:
+        """Host buffers (pinned for speed); returns with the outputs in `out`."""
+        _check(lib().kivi_decode_layers_host(self._arr, len(self.caches), _hptr(q), _hptr(t_k),
+                                             _hptr(t_v), int(q_per_kv), _hptr(out),
+                                             int(bool(scale_logits)),
+                                             _stream_ptr(stream, self.device)))
+
+
+class Projection:
+    """One layer's q/k/v projection (reference workload.cpp:230-232, x @ W) on
+    the tcgen05 tensor cores in 3xTF32, optionally fused with the KV-cache
+    append (kivi_proj_append).  w_q, w_k, w_v: [hidden_in, hidden_out] fp32
+    CUDA tensors (copied and transposed once)."""
+
+    def __init__(self, w_q, w_k, w_v):
+        self.hidden_in, self.hidden_out = int(w_q.shape[0]), int(w_q.shape[1])
+        self.device = w_q.device.index
+        h = ctypes.c_void_p()
+        _check(lib().kivi_proj_create(self.device, self.hidden_in, self.hidden_out,
+                                      _dptr(w_q.contiguous(), self.device),
+                                      _dptr(w_k.contiguous(), self.device),
+                                      _dptr(w_v.contiguous(), self.device),
+                                      _stream_ptr(None, self.device), ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().kivi_proj_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def gemm(self, x, seq: int = 0):
+        """x: [n, hidden_in] -> (q, k, v) [n, hidden_out]; seq > 0: per-unit
+        [n // seq * heads, seq, 128] (the layout KVCache.prefill takes)."""
+        torch = _torch()
+        n = int(x.shape[0])
+        shape = (n, self.hidden_out) if seq == 0 else \
+            (n // seq * (self.hidden_out // 128), seq, 128)
+        outs = [torch.empty(shape, device=x.device, dtype=torch.float32) for _ in range(3)]
+        dv = self.device
+        _check(lib().kivi_proj_gemm(self._h, _dptr(x.contiguous(), dv), n,
+                                    *[_dptr(o, dv) for o in outs], int(seq),
+                                    _stream_ptr(None, dv)))
+        return tuple(outs)
+
+    def append(self, cache, x, q_out=None):
+        """Projection of the decode token rows x [n, hidden_in] fused with the
+        append into `cache` (n * heads units); returns q [n * heads, 1, 128]."""
+        torch = _torch()
+        n = int(x.shape[0])
+        if q_out is None:
+            q_out = torch.empty((n * (self.hidden_out // 128), 1, 128), device=x.device,
+                                dtype=torch.float32)
+        dv = self.device
+        _check(lib().kivi_proj_append(self._h, cache._h, _dptr(x.contiguous(), dv), n,
+                                      _dptr(q_out, dv), _stream_ptr(None, dv)))
+        return q_out
+
+
+def step_graph_stats(device=None) -> dict:
+    """kivi_step_graph_stats of this thread on `device` (default: current)."""
+    torch = _torch()
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        _check(lib().kivi_step_graph_stats(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"replayed": a.value, "reinstantiated": b.value, "capture_failed": c.value}
 
 
 def _hptr(a):

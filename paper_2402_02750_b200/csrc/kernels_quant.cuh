@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
 // thread per (unit, 32-token tile, channel) group: lanes are 32 consecutive
 // channels, so every token row is one coalesced 128-byte load per warp and the
 // group's code words one contiguous store.  The ring's last row (token l) is
-// read from t_k, which the append warps write concurrently.
+// read from t_k, which the append warps write concurrently; with t_k == NULL
+// (n_app = 0: the projection kernel already wrote the row) from the ring.
 template <int B>
 __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
                                                                 const float* __restrict__ tk,
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         const int r = tl * G + i;
-        x[i] = r == last ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
+        x[i] = (r == last && tk) ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
     }
     uint32_t w[B];
     const float2 lh = key_group_fast<B>(x, w);

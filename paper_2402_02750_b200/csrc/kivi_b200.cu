@@ -16,6 +16,7 @@
 #include "kernels_attend_gqa_tc.cuh"
 #include "kernels_attend_generic.cuh"
 #include "kernels_quant.cuh"
+#include "kernels_project.cuh"
 
 using namespace kivi_b200;
 
@@ -321,7 +322,7 @@ int env_int(const char* name, int dflt) {
 struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
-    int gqa_tc, gqa_partial, gqa_tail_ctas;
+    int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -340,6 +341,7 @@ struct Tuning {
         gqa_tc = env_int("KIVI_GQA_TC", 1);
         gqa_partial = env_int("KIVI_GQA_PARTIAL", 1);
         gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
+        step_graph = env_int("KIVI_STEP_GRAPH", 0);
     }
 };
 Tuning g_tune;
@@ -1396,6 +1398,447 @@ kivi_status kivi_decode_host(kivi_cache* h, const float* t_q, const float* t_k, 
         KIVI_CUDA(cudaMemcpyAsync(weights, sg->w, sizeof(float) * wlen, cudaMemcpyDeviceToHost,
                                   h->d2h));
     KIVI_CUDA(cudaEventRecord(sg->out_free, h->d2h));
+    return KIVI_OK;
+}
+
+// ---- one decode step of a whole model (one cache per layer) -----------------
+
+static kivi_status check_layers(kivi_cache* const* caches, int32_t n_layers) {
+    if (!caches || n_layers < 1) return fail(KIVI_ERR_USAGE, "decode_layers: no caches");
+    for (int32_t i = 0; i < n_layers; ++i) {
+        const kivi_cache* c = caches[i];
+        if (!c) return fail(KIVI_ERR_USAGE, "decode_layers: cache %d is NULL", i);
+        const kivi_cache* c0 = caches[0];
+        if (c->n_units != c0->n_units || c->device != c0->device ||
+            c->cfg.head_dim != c0->cfg.head_dim)
+            return fail(KIVI_ERR_SHAPE, "decode_layers: cache %d differs in units/device/head_dim",
+                        i);
+    }
+    return KIVI_OK;
+}
+
+static kivi_status decode_layers_enqueue(kivi_cache* const* caches, int32_t n_layers,
+                                         const float* t_q, const float* t_k, const float* t_v,
+                                         int32_t q_per_kv, float* out, int32_t scale_logits,
+                                         void* stream) {
+    const int64_t U = caches[0]->n_units, d = caches[0]->cfg.head_dim;
+    const int64_t qrow = U * q_per_kv * d, krow = U * d;
+    for (int32_t i = 0; i < n_layers; ++i) {
+        kivi_status rc = kivi_decode(caches[i], t_q + i * qrow, t_k + i * krow, t_v + i * krow,
+                                     q_per_kv, out + i * qrow, nullptr, scale_logits, stream);
+        if (rc) return rc;
+    }
+    return KIVI_OK;
+}
+
+kivi_status kivi_decode_layers(kivi_cache* const* caches, int32_t n_layers, const float* t_q,
+                               const float* t_k, const float* t_v, int32_t q_per_kv, float* out,
+                               int32_t scale_logits, void* stream) {
+    kivi_status rc = check_layers(caches, n_layers);
+    if (rc) return rc;
+    if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
+    if (!t_q || !t_k || !t_v || !out) return fail(KIVI_ERR_SHAPE, "decode_layers: NULL rows");
+    DeviceGuard g(caches[0]->device);
+    return decode_layers_enqueue(caches, n_layers, t_q, t_k, t_v, q_per_kv, out, scale_logits,
+                                 stream);
+}
+
+namespace {
+// Device staging of kivi_decode_layers_host, one per (host thread, device):
+// the step's rows for every layer, uploaded in three copies.  Optionally the
+// whole step (uploads, every layer's kernels, the result copy) is captured as
+// a CUDA graph and replayed: re-captured every step (the kernels' arguments
+// follow l) and applied to the instantiated graph with cudaGraphExecUpdate,
+// re-instantiated only when the launch topology changes.
+struct StepStage {
+    float* q = nullptr;
+    float* k = nullptr;
+    float* v = nullptr;
+    float* out = nullptr;
+    int64_t cap_q = 0, cap_k = 0, cap_v = 0, cap_out = 0;
+    // layer i's rows go up on h2d (gated by ev_in[i]) while earlier layers
+    // compute; its output comes back on d2h after ev_out[i]
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_out;
+    cudaEvent_t ev_start = nullptr, ev_join = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t graph_steps = 0, graph_updates_failed = 0, graph_capture_failed = 0;
+    cudaError_t init(int n_layers) {
+        cudaError_t e = cudaSuccess;
+        if (!h2d) {
+            if ((e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking))) return e;
+            if ((e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking))) return e;
+            if ((e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming))) return e;
+            if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
+        }
+        while ((int)ev_in.size() < n_layers) {
+            cudaEvent_t a = nullptr, b = nullptr;
+            if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming))) return e;
+            if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming))) return e;
+            ev_in.push_back(a);
+            ev_out.push_back(b);
+        }
+        return e;
+    }
+    ~StepStage() {
+        cudaFree(q);
+        cudaFree(k);
+        cudaFree(v);
+        cudaFree(out);
+        for (auto e : ev_in) cudaEventDestroy(e);
+        for (auto e : ev_out) cudaEventDestroy(e);
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+StepStage& step_stage() {
+    thread_local StepStage s[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    return s[dev];
+}
+}  // namespace
+
+kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers, const float* t_q,
+                                    const float* t_k, const float* t_v, int32_t q_per_kv,
+                                    float* out, int32_t scale_logits, void* stream) {
+    kivi_status rc = check_layers(caches, n_layers);
+    if (rc) return rc;
+    if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
+    if (!t_q || !t_k || !t_v || !out) return fail(KIVI_ERR_SHAPE, "decode_layers: NULL rows");
+    DeviceGuard g(caches[0]->device);
+    const int64_t U = caches[0]->n_units, d = caches[0]->cfg.head_dim;
+    const int64_t nq = n_layers * U * q_per_kv * d, nk = n_layers * U * d;
+    StepStage& sg = step_stage();
+    if ((rc = ensure(&sg.q, &sg.cap_q, nq))) return rc;
+    if ((rc = ensure(&sg.k, &sg.cap_k, nk))) return rc;
+    if ((rc = ensure(&sg.v, &sg.cap_v, nk))) return rc;
+    if ((rc = ensure(&sg.out, &sg.cap_out, nq))) return rc;
+    // A step that grows a cache (capacity doubling also regrows its partial
+    // buffers) runs directly: allocations are not allowed inside a capture.
+    bool grows = false;
+    for (int32_t i = 0; i < n_layers; ++i) {
+        grows |= caches[i]->l + 1 > caches[i]->cap;
+        rc = ensure_capacity(caches[i], caches[i]->l + 1, S(stream));
+        if (rc) return rc;
+    }
+    KIVI_CUDA(sg.init(n_layers));
+    cudaStream_t st = S(stream);
+    const int64_t qrow = U * q_per_kv * d, krow = U * d;
+    auto enqueue = [&]() -> kivi_status {
+        if (n_layers == 1) {
+            // one layer: nothing to overlap the copies with; one stream
+            // avoids the cross-stream event latencies (C1: a ~25 us step)
+            KIVI_CUDA(cudaMemcpyAsync(sg.q, t_q, sizeof(float) * qrow, cudaMemcpyHostToDevice, st));
+            KIVI_CUDA(cudaMemcpyAsync(sg.k, t_k, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
+            KIVI_CUDA(cudaMemcpyAsync(sg.v, t_v, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
+            kivi_status r = kivi_decode(caches[0], sg.q, sg.k, sg.v, q_per_kv, sg.out, nullptr,
+                                        scale_logits, stream);
+            if (r) return r;
+            KIVI_CUDA(cudaMemcpyAsync(out, sg.out, sizeof(float) * qrow, cudaMemcpyDeviceToHost, st));
+            return KIVI_OK;
+        }
+        // fork the copy streams off `stream` (this call's work starts after
+        // what the caller enqueued before it)
+        KIVI_CUDA(cudaEventRecord(sg.ev_start, st));
+        KIVI_CUDA(cudaStreamWaitEvent(sg.h2d, sg.ev_start, 0));
+        KIVI_CUDA(cudaStreamWaitEvent(sg.d2h, sg.ev_start, 0));
+        for (int32_t i = 0; i < n_layers; ++i) {
+            KIVI_CUDA(cudaMemcpyAsync(sg.q + i * qrow, t_q + i * qrow, sizeof(float) * qrow,
+                                      cudaMemcpyHostToDevice, sg.h2d));
+            KIVI_CUDA(cudaMemcpyAsync(sg.k + i * krow, t_k + i * krow, sizeof(float) * krow,
+                                      cudaMemcpyHostToDevice, sg.h2d));
+            KIVI_CUDA(cudaMemcpyAsync(sg.v + i * krow, t_v + i * krow, sizeof(float) * krow,
+                                      cudaMemcpyHostToDevice, sg.h2d));
+            KIVI_CUDA(cudaEventRecord(sg.ev_in[i], sg.h2d));
+        }
+        for (int32_t i = 0; i < n_layers; ++i) {
+            KIVI_CUDA(cudaStreamWaitEvent(st, sg.ev_in[i], 0));
+            kivi_status r = kivi_decode(caches[i], sg.q + i * qrow, sg.k + i * krow,
+                                        sg.v + i * krow, q_per_kv, sg.out + i * qrow, nullptr,
+                                        scale_logits, stream);
+            if (r) return r;
+            KIVI_CUDA(cudaEventRecord(sg.ev_out[i], st));
+            KIVI_CUDA(cudaStreamWaitEvent(sg.d2h, sg.ev_out[i], 0));
+            KIVI_CUDA(cudaMemcpyAsync(out + i * qrow, sg.out + i * qrow, sizeof(float) * qrow,
+                                      cudaMemcpyDeviceToHost, sg.d2h));
+        }
+        // join: `stream` ends after the last result copy
+        KIVI_CUDA(cudaEventRecord(sg.ev_join, sg.d2h));
+        KIVI_CUDA(cudaStreamWaitEvent(st, sg.ev_join, 0));
+        return KIVI_OK;
+    };
+    bool profiling = false;
+    for (int32_t i = 0; i < n_layers; ++i) profiling |= caches[i]->profile;
+    if (tune().step_graph && st != nullptr && !profiling && !grows) {
+        // The partial-result buffers must already exist (an allocation inside
+        // a capture invalidates it): the first call of a cache runs directly.
+        bool warm = true;
+        for (int32_t i = 0; i < n_layers; ++i) warm &= caches[i]->part_o != nullptr;
+        if (warm) {
+            std::vector<int64_t> l0(n_layers), kc(n_layers), vc(n_layers), ws(n_layers);
+            for (int32_t i = 0; i < n_layers; ++i) {
+                l0[i] = caches[i]->l;
+                kc[i] = caches[i]->kres_cap;
+                vc[i] = caches[i]->vres_cap;
+                ws[i] = caches[i]->work_seq;
+            }
+            KIVI_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            kivi_status r = enqueue();
+            cudaGraph_t graph = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            if (r == KIVI_OK && ce == cudaSuccess && graph) {
+                bool ok = false;
+                if (sg.exec) {
+                    cudaGraphExecUpdateResultInfo info{};
+                    ok = cudaGraphExecUpdate(sg.exec, graph, &info) == cudaSuccess;
+                    if (!ok) {
+                        cudaGetLastError();
+                        cudaGraphExecDestroy(sg.exec);
+                        sg.exec = nullptr;
+                        sg.graph_updates_failed++;
+                    }
+                }
+                if (!ok) ok = cudaGraphInstantiate(&sg.exec, graph, 0) == cudaSuccess;
+                cudaGraphDestroy(graph);
+                if (ok) {
+                    KIVI_CUDA(cudaGraphLaunch(sg.exec, st));
+                    KIVI_CUDA(cudaStreamSynchronize(st));
+                    sg.graph_steps++;
+                    return KIVI_OK;
+                }
+            }
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            // capture failed: undo the host-side step bookkeeping and run directly
+            if (getenv("KIVI_DEBUG_GRAPH"))
+                fprintf(stderr, "kivi: step graph capture failed (%s / %s); direct launch\n",
+                        r ? g_last_error.c_str() : "ok", cudaGetErrorString(ce));
+            sg.graph_capture_failed++;
+            for (int32_t i = 0; i < n_layers; ++i) {
+                caches[i]->l = l0[i];
+                caches[i]->kres_cap = kc[i];
+                caches[i]->vres_cap = vc[i];
+                caches[i]->work_seq = ws[i];
+            }
+        }
+    }
+    rc = enqueue();
+    if (rc) return rc;
+    KIVI_CUDA(cudaStreamSynchronize(st));
+    return KIVI_OK;
+}
+
+// ---- q/k/v projection on the tensor cores (kernels_project.cuh) ------------
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D fp32 tensor map over a row-major [rows][cols] matrix, box [box_rows][32]
+// with 128-byte swizzle (rows past `rows` read as zeros).
+kivi_status make_tmap(CUtensorMap* tm, const float* base, int64_t rows, int64_t cols,
+                      int box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return fail(KIVI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+    const cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KIVI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return KIVI_OK;
+}
+
+__global__ void transpose_kernel(const float* __restrict__ in, int64_t rows, int64_t cols,
+                                 float* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+}  // namespace
+
+struct kivi_proj {
+    int device = 0;
+    int64_t hidden_in = 0, hidden_out = 0;
+    float* wt[3] = {nullptr, nullptr, nullptr};  // W^T: [hidden_out][hidden_in]
+    CUtensorMap tm_w[3];
+    int64_t launches = 0;
+};
+
+kivi_status kivi_proj_create(int device, int64_t hidden_in, int64_t hidden_out, const float* w_q,
+                             const float* w_k, const float* w_v, void* stream, kivi_proj** out) {
+    if (!out) return fail(KIVI_ERR_USAGE, "out is NULL");
+    *out = nullptr;
+    if (hidden_in < 32 || hidden_in % 32 != 0 || hidden_out < 128 || hidden_out % 128 != 0)
+        return fail(KIVI_ERR_SHAPE,
+                    "projection: hidden_in must be a multiple of 32 and hidden_out of 128 "
+                    "(got %lld, %lld)",
+                    (long long)hidden_in, (long long)hidden_out);
+    if (!w_q || !w_k || !w_v) return fail(KIVI_ERR_USAGE, "projection: NULL weights");
+    DeviceGuard g(device);
+    kivi_proj* p = new kivi_proj();
+    p->device = device;
+    p->hidden_in = hidden_in;
+    p->hidden_out = hidden_out;
+    const float* w[3] = {w_q, w_k, w_v};
+    cudaStream_t st = S(stream);
+    for (int i = 0; i < 3; ++i) {
+        if (dalloc(&p->wt[i], (size_t)(hidden_in * hidden_out)) != cudaSuccess) {
+            kivi_proj_destroy(p);
+            return fail(KIVI_ERR_OOM, "projection: weight allocation failed");
+        }
+        dim3 grid((unsigned)ceil_div(hidden_out, 32), (unsigned)ceil_div(hidden_in, 32));
+        transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(w[i], hidden_in, hidden_out, p->wt[i]);
+        kivi_status rc = make_tmap(&p->tm_w[i], p->wt[i], hidden_out, hidden_in, proj::BM);
+        if (rc) {
+            kivi_proj_destroy(p);
+            return rc;
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        kivi_proj_destroy(p);
+        return fail(KIVI_ERR_CUDA, "projection: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return KIVI_OK;
+}
+
+kivi_status kivi_proj_destroy(kivi_proj* p) {
+    if (!p) return KIVI_OK;
+    DeviceGuard g(p->device);
+    for (auto w : p->wt) cudaFree(w);
+    delete p;
+    return KIVI_OK;
+}
+
+namespace {
+// One launch of proj_kernel over rows [0, n) of x (N tiles of <= 256 rows).
+kivi_status launch_proj(kivi_proj* p, const float* x, int64_t n, proj::ProjArgs a, int bits,
+                        cudaStream_t st) {
+    if (n < 1) return fail(KIVI_ERR_SHAPE, "projection: no rows");
+    const int N = (int)std::min<int64_t>(256, round_up(n, 16));
+    CUtensorMap tm_x;
+    kivi_status rc = make_tmap(&tm_x, x, n, p->hidden_in, N);
+    if (rc) return rc;
+    const int a_bytes = proj::BM * proj::BK * 4, b_bytes = N * proj::BK * 4;
+    const int stage = 2 * a_bytes + 2 * b_bytes;
+    const int nkb = (int)(p->hidden_in / proj::BK);
+    a.K = (int)p->hidden_in;
+    a.N = N;
+    a.tiles_m = (int)(p->hidden_out / proj::BM);
+    a.stages = std::max(2, std::min(std::min(6, nkb), proj::SMEM_LIMIT / stage));
+    a.hidden_out = (int)p->hidden_out;
+    const size_t smem = 1024 + (size_t)a.stages * stage + (3 * a.stages + 2) * 8;
+    auto kern = bits == 4 ? proj::proj_kernel<4> : proj::proj_kernel<2>;
+    KIVI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int n_tiles = (int)ceil_div(n, N);
+    for (int t = 0; t < n_tiles; ++t) {  // one launch per N tile (n_valid / n_tile0 differ)
+        proj::ProjArgs at = a;
+        at.n_tile0 = t * N;
+        at.n_valid = (int)std::min<int64_t>(N, n - (int64_t)t * N);
+        kern<<<dim3((unsigned)(3 * at.tiles_m)), proj::THREADS, smem, st>>>(
+            p->tm_w[0], p->tm_w[1], p->tm_w[2], tm_x, at);
+        KIVI_LAUNCHED();
+        p->launches++;
+    }
+    return KIVI_OK;
+}
+}  // namespace
+
+kivi_status kivi_proj_gemm(kivi_proj* p, const float* x, int64_t n, float* out_q, float* out_k,
+                           float* out_v, int64_t seq, void* stream) {
+    if (!p || !x) return fail(KIVI_ERR_USAGE, "projection: NULL argument");
+    if (!out_q || !out_k || !out_v) return fail(KIVI_ERR_USAGE, "projection: NULL output");
+    if (seq < 0 || (seq > 0 && (n % seq != 0 || p->hidden_out % 128 != 0)))
+        return fail(KIVI_ERR_SHAPE, "projection: rows must be a multiple of seq");
+    DeviceGuard g(p->device);
+    proj::ProjArgs a{};
+    a.mode = seq > 0 ? 2 : 0;
+    a.seq = (int)seq;
+    a.heads = (int)(p->hidden_out / proj::BM);
+    a.out[0] = out_q;
+    a.out[1] = out_k;
+    a.out[2] = out_v;
+    return launch_proj(p, x, n, a, 2, S(stream));
+}
+
+kivi_status kivi_proj_append(kivi_proj* p, kivi_cache* h, const float* x, int64_t n, float* q_out,
+                             void* stream) {
+    if (!p || !h || !x || !q_out) return fail(KIVI_ERR_USAGE, "projection: NULL argument");
+    const kivi_config& cf = h->cfg;
+    if (cf.head_dim != 128 || cf.group_size != 32 || (cf.bits != 2 && cf.bits != 4))
+        return fail(KIVI_ERR_CONFIG,
+                    "fused projection-append needs head_dim 128, group 32, 2 or 4 bits");
+    const int64_t heads = p->hidden_out / proj::BM;
+    if (h->n_units != n * heads)
+        return fail(KIVI_ERR_SHAPE, "projection: cache has %lld units, rows x heads = %lld",
+                    (long long)h->n_units, (long long)(n * heads));
+    if (h->device != p->device) return fail(KIVI_ERR_USAGE, "projection and cache on different devices");
+    DeviceGuard g(p->device);
+    cudaStream_t st = S(stream);
+    kivi_status rc = ensure_capacity(h, h->l + 1, st);
+    if (rc) return rc;
+    proj::ProjArgs a{};
+    a.mode = 1;
+    a.out[0] = q_out;
+    a.c = h->dev;
+    a.l = h->l;
+    a.heads = (int)heads;
+    rc = launch_proj(p, x, n, a, cf.bits, st);
+    if (rc) return rc;
+    h->total_launches += ceil_div(n, 256);
+    if ((h->l + 1) % cf.residual_length == 0) {
+        // key flush of this step: the projection wrote token l into the ring
+        const int64_t groups = h->n_units * (cf.residual_length / 32) * 128;
+        const unsigned fgrid = (unsigned)ceil_div(groups, 256);
+        if (cf.bits == 2)
+            append_flush_fast_kernel<2><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0);
+        else
+            append_flush_fast_kernel<4><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0);
+        KIVI_LAUNCHED();
+        h->total_launches++;
+    }
+    append_bookkeeping(h);
+    return KIVI_OK;
+}
+
+kivi_status kivi_step_graph_stats(int64_t* replayed, int64_t* reinstantiated,
+                                  int64_t* capture_failed) {
+    StepStage& sg = step_stage();
+    if (replayed) *replayed = sg.graph_steps;
+    if (reinstantiated) *reinstantiated = sg.graph_updates_failed;
+    if (capture_failed) *capture_failed = sg.graph_capture_failed;
     return KIVI_OK;
 }
 

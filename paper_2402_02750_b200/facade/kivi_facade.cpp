@@ -6,17 +6,27 @@
 // the reference's exception types and messages), moves data, and keeps the
 // caller-owned states in the reference layout.
 //
-// State model: KeyCacheState / ValueCacheState remain plain values.  Each
-// call loads the unit into a per-thread device cache (kivi_import_unit), runs
-// the kernels, and writes the new state back (kivi_export_unit).  The batched
-// C-ABI (one kivi_cache for a whole layer, state resident in HBM) is the
-// high-throughput path; this facade is the drop-in for single-unit callers.
+// State model (device-resident).  KeyCacheState / ValueCacheState stay plain
+// caller-owned values (reference kv_cache.hpp:22-35), but the grouped store of
+// a state produced here lives in HBM: a per-state-pair single-unit kivi_cache
+// (a "Mirror") holds the codes, (lo, hi) pairs and residual rings, and the
+// states' QuantizedTensors hold an immutable DeviceView of it whose host
+// vectors (packed() / zero_points() / scales()) are downloaded only when read.
+// The residual rows (public Matrix fields) are kept on the host as well,
+// updated by the reference's own rules (kv_cache.cpp:66-98) from the rows the
+// caller passed in.  A call on a state that is still the mirror's latest
+// output uploads only the new token's rows (and q) and downloads only the
+// output and softmax weights; any other state (hand-built, copied and
+// diverged, edited) is imported in full first.  Copies share a view
+// (copy-on-write: a view someone else still holds is downloaded before the
+// mirror moves on).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -41,10 +51,27 @@ struct TensorAccess {
         t.cols_ = cols;
         return t;
     }
+    static QuantizedTensor make_view(std::shared_ptr<const DeviceView> v, Index rows, Index cols,
+                                     const QuantParams& p) {
+        QuantizedTensor t(p);
+        t.dev_ = std::move(v);
+        t.rows_ = rows;
+        t.cols_ = cols;
+        return t;
+    }
     static std::vector<std::uint8_t>& packed(QuantizedTensor& t) { return t.packed_; }
     static std::vector<double>& zeros(QuantizedTensor& t) { return t.zero_points_; }
     static std::vector<double>& scales(QuantizedTensor& t) { return t.scales_; }
     static Index& rows(QuantizedTensor& t) { return t.rows_; }
+    static const std::shared_ptr<const DeviceView>& view(const QuantizedTensor& t) { return t.dev_; }
+    // Host-owned data again (before a host-side mutation such as concat_tokens).
+    static void own(QuantizedTensor& t) {
+        if (!t.dev_) return;
+        t.packed_ = view_packed(*t.dev_);
+        t.zero_points_ = view_zero_points(*t.dev_);
+        t.scales_ = view_scales(*t.dev_);
+        t.dev_.reset();
+    }
 };
 }  // namespace detail
 
@@ -141,30 +168,188 @@ kivi_axis axis_of(Axis a) { return a == Axis::per_channel ? KIVI_PER_CHANNEL : K
 
 std::size_t packed_size(std::uint64_t codes, int bits) { return (codes * bits + 7) / 8; }
 
-// ---- per-thread device cache pool (one single-unit kivi_cache per config) --
-struct CacheDeleter {
-    void operator()(kivi_cache* c) const { kivi_cache_destroy(c); }
-};
-using CacheKey = std::tuple<int, Index, Index, Index>;
+// ---- device-resident cache states --------------------------------------------
 
-kivi_cache* pooled_cache(const CacheConfig& cfg) {
-    thread_local std::map<CacheKey, std::unique_ptr<kivi_cache, CacheDeleter>> pool;
-    const CacheKey key{cfg.bits, cfg.group_size, cfg.residual_length, cfg.head_dim};
-    auto it = pool.find(key);
-    if (it != pool.end()) return it->second.get();
-    kivi_config c{cfg.bits, cfg.group_size, cfg.residual_length, cfg.head_dim};
-    kivi_cache* h = nullptr;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    check(kivi_cache_create(&c, dev, 1, 0, &h));
-    check(kivi_set_attend_path(h, 1));  // reference arithmetic order (generic kernel)
-    pool.emplace(key, std::unique_ptr<kivi_cache, CacheDeleter>(h));
-    return h;
+// Pinned staging for the per-call rows of one host thread (q, k, v in; output
+// and softmax weights out): the copies are asynchronous, one sync per call.
+struct Pinned {
+    float* p = nullptr;
+    std::size_t cap = 0;
+    float* get(std::size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            std::size_t want = 4096;
+            while (want < n) want <<= 1;
+            cuda(cudaHostAlloc(reinterpret_cast<void**>(&p), want * sizeof(float),
+                               cudaHostAllocDefault),
+                 "cudaHostAlloc");
+            cap = want;
+        }
+        return p;
+    }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+Pinned& pinned(int slot) {
+    thread_local Pinned p[2];
+    return p[slot];
 }
 
-// Loads a caller-owned state pair into the device cache.
-void load_state(kivi_cache* h, const KeyCacheState& ks, const ValueCacheState& vs,
-                const CacheConfig& cfg) {
+cudaStream_t facade_stream() {
+    thread_local cudaStream_t s = nullptr;
+    if (!s) cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    return s;
+}
+
+}  // namespace
+
+namespace detail {
+
+// One state pair's cache in HBM: a single-unit kivi_cache.  `version` counts
+// the mutations; the views of the current version are the only ones whose
+// data is still on the device.
+struct Mirror {
+    kivi_cache* h = nullptr;
+    CacheConfig cfg;
+    std::uint64_t version = 0;
+    std::weak_ptr<DeviceView> kview, vview;
+    Matrix kres, vres;  // the residual rows last handed to the states
+    std::mutex mu;
+    ~Mirror() {
+        if (h) kivi_cache_destroy(h);
+    }
+};
+
+struct DeviceView {
+    std::shared_ptr<Mirror> m;
+    std::uint64_t version = 0;
+    bool key = true;
+    mutable std::once_flag once;
+    mutable std::vector<std::uint8_t> packed;
+    mutable std::vector<double> zeros, scales;
+
+    // Downloads this view's grouped store (valid while the mirror is still at
+    // `version`; fetch_shared() runs before every mutation of a shared view).
+    void fetch() const {
+        std::call_once(once, [&] {
+            std::lock_guard<std::mutex> lk(m->mu);
+            if (m->version != version)
+                throw std::logic_error("kivi facade: stale device view");
+            kivi_cache_info info{};
+            check(kivi_cache_get_info(m->h, &info));
+            const Index d = m->cfg.head_dim, G = m->cfg.group_size;
+            const Index rows = key ? info.key_grouped_tokens : info.value_grouped_tokens;
+            packed.assign(packed_size((std::uint64_t)rows * d, m->cfg.bits), 0);
+            zeros.assign(rows * d / G, 0.0);
+            scales.assign(rows * d / G, 0.0);
+            kivi_unit_state st{};
+            if (key) {
+                st.key_packed = packed.data();
+                st.key_zero = zeros.data();
+                st.key_scale = scales.data();
+            } else {
+                st.value_packed = packed.data();
+                st.value_zero = zeros.data();
+                st.value_scale = scales.data();
+            }
+            check(kivi_export_unit(m->h, 0, &st, facade_stream()));
+        });
+    }
+};
+
+const std::vector<std::uint8_t>& view_packed(const DeviceView& v) {
+    v.fetch();
+    return v.packed;
+}
+const std::vector<double>& view_zero_points(const DeviceView& v) {
+    v.fetch();
+    return v.zeros;
+}
+const std::vector<double>& view_scales(const DeviceView& v) {
+    v.fetch();
+    return v.scales;
+}
+
+}  // namespace detail
+
+namespace {
+
+using detail::DeviceView;
+using detail::Mirror;
+
+bool same_cfg(const CacheConfig& a, const CacheConfig& b) {
+    return a.bits == b.bits && a.group_size == b.group_size &&
+           a.residual_length == b.residual_length && a.head_dim == b.head_dim;
+}
+
+bool same_matrix(const Matrix& a, const Matrix& b) {
+    return a.rows() == b.rows() && a.cols() == b.cols() &&
+           (a.size() == 0 || std::memcmp(a.data(), b.data(), sizeof(float) * a.size()) == 0);
+}
+
+std::shared_ptr<Mirror> new_mirror(const CacheConfig& cfg, Index capacity) {
+    auto m = std::make_shared<Mirror>();
+    m->cfg = cfg;
+    kivi_config c{cfg.bits, cfg.group_size, cfg.residual_length, cfg.head_dim};
+    int dev = 0;
+    cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    check(kivi_cache_create(&c, dev, 1, capacity, &m->h));
+    return m;
+}
+
+// The mirror whose latest output these states are, or nullptr.
+std::shared_ptr<Mirror> current_mirror(const KeyCacheState& ks, const ValueCacheState& vs,
+                                       const CacheConfig& cfg) {
+    const auto& kv = detail::TensorAccess::view(ks.grouped);
+    const auto& vv = detail::TensorAccess::view(vs.grouped);
+    if (!kv || !vv || kv->m != vv->m || !kv->key || vv->key) return nullptr;
+    const std::shared_ptr<Mirror>& m = kv->m;
+    if (kv->version != m->version || vv->version != m->version || !same_cfg(m->cfg, cfg))
+        return nullptr;
+    kivi_cache_info info{};
+    check(kivi_cache_get_info(m->h, &info));
+    if (ks.total_tokens != info.total_tokens || vs.total_tokens != info.total_tokens ||
+        ks.residual_capacity != info.key_residual_capacity ||
+        vs.residual_capacity != info.value_residual_capacity ||
+        ks.grouped.rows() != info.key_grouped_tokens || vs.grouped.rows() != info.value_grouped_tokens)
+        return nullptr;
+    if (!same_matrix(ks.residual, m->kres) || !same_matrix(vs.residual, m->vres)) return nullptr;
+    return m;
+}
+
+// Publishes the mirror's current device state into the caller's states: new
+// views of the grouped stores; residual rows and counters on the host.
+void publish(const std::shared_ptr<Mirror>& m, KeyCacheState& ks, ValueCacheState& vs) {
+    kivi_cache_info info{};
+    check(kivi_cache_get_info(m->h, &info));
+    auto kv = std::make_shared<DeviceView>();
+    kv->m = m;
+    kv->version = m->version;
+    kv->key = true;
+    auto vv = std::make_shared<DeviceView>();
+    vv->m = m;
+    vv->version = m->version;
+    vv->key = false;
+    m->kview = kv;
+    m->vview = vv;
+    const Index d = m->cfg.head_dim;
+    ks.grouped = detail::TensorAccess::make_view(kv, info.key_grouped_tokens, d, m->cfg.key_params());
+    vs.grouped =
+        detail::TensorAccess::make_view(vv, info.value_grouped_tokens, d, m->cfg.value_params());
+    ks.residual = m->kres;
+    vs.residual = m->vres;
+    ks.total_tokens = vs.total_tokens = info.total_tokens;
+    ks.residual_capacity = info.key_residual_capacity;
+    vs.residual_capacity = info.value_residual_capacity;
+}
+
+// Imports a state pair in the reference layout into a fresh mirror (full
+// upload: the states were not produced by this facade, or diverged).
+std::shared_ptr<Mirror> import_states(const KeyCacheState& ks, const ValueCacheState& vs,
+                                      const CacheConfig& cfg) {
     const Index l = ks.total_tokens;
     const Index R = cfg.residual_length;
     if (vs.total_tokens != l)
@@ -173,43 +358,59 @@ void load_state(kivi_cache* h, const KeyCacheState& ks, const ValueCacheState& v
     if (ks.grouped.rows() != l - kr || ks.residual.rows() != kr || vs.grouped.rows() != l - vr ||
         vs.residual.rows() != vr)
         throw UsageError("kivi facade: state is not a prefill/append_token state");
+    auto m = new_mirror(cfg, l + R);
     kivi_unit_state st{};
-    auto& kq = const_cast<QuantizedTensor&>(ks.grouped);
-    auto& vq = const_cast<QuantizedTensor&>(vs.grouped);
-    st.key_packed = TensorAccess::packed(kq).data();
-    st.key_zero = TensorAccess::zeros(kq).data();
-    st.key_scale = TensorAccess::scales(kq).data();
+    st.key_packed = const_cast<std::uint8_t*>(ks.grouped.packed().data());
+    st.key_zero = const_cast<double*>(ks.grouped.zero_points().data());
+    st.key_scale = const_cast<double*>(ks.grouped.scales().data());
     st.key_residual = const_cast<float*>(ks.residual.data());
-    st.value_packed = TensorAccess::packed(vq).data();
-    st.value_zero = TensorAccess::zeros(vq).data();
-    st.value_scale = TensorAccess::scales(vq).data();
+    st.value_packed = const_cast<std::uint8_t*>(vs.grouped.packed().data());
+    st.value_zero = const_cast<double*>(vs.grouped.zero_points().data());
+    st.value_scale = const_cast<double*>(vs.grouped.scales().data());
     st.value_residual = const_cast<float*>(vs.residual.data());
-    check(kivi_import_unit(h, 0, l, ks.residual_capacity, vs.residual_capacity, &st, nullptr));
+    check(kivi_import_unit(m->h, 0, l, ks.residual_capacity, vs.residual_capacity, &st,
+                           facade_stream()));
+    m->kres = ks.residual;
+    m->vres = vs.residual;
+    return m;
 }
 
-// Writes the device cache's unit back into the caller-owned states.
-void store_state(kivi_cache* h, KeyCacheState& ks, ValueCacheState& vs, const CacheConfig& cfg) {
-    kivi_cache_info info{};
-    check(kivi_cache_get_info(h, &info));
-    const Index d = cfg.head_dim, G = cfg.group_size;
-    const int B = cfg.bits;
-    const Index kg = info.key_grouped_tokens, vg = info.value_grouped_tokens;
-    std::vector<std::uint8_t> kp(packed_size((std::uint64_t)kg * d, B)),
-        vp(packed_size((std::uint64_t)vg * d, B));
-    std::vector<double> kz(kg * d / G), ksc(kg * d / G), vz(vg * d / G), vsc(vg * d / G);
-    Matrix kres(info.key_residual_rows, d), vres(info.value_residual_rows, d);
-    kivi_unit_state st{kp.data(), kz.data(), ksc.data(), kres.data(),
-                       vp.data(), vz.data(), vsc.data(), vres.data()};
-    check(kivi_export_unit(h, 0, &st, nullptr));
-    ks.grouped = TensorAccess::make(std::move(kp), std::move(kz), std::move(ksc), kg, d,
-                                    cfg.key_params());
-    vs.grouped = TensorAccess::make(std::move(vp), std::move(vz), std::move(vsc), vg, d,
-                                    cfg.value_params());
-    ks.residual = std::move(kres);
-    vs.residual = std::move(vres);
-    ks.total_tokens = vs.total_tokens = info.total_tokens;
-    ks.residual_capacity = info.key_residual_capacity;
-    vs.residual_capacity = info.value_residual_capacity;
+// The mirror these states can be advanced on: their own (no copy) when they
+// are its latest output, else a fresh import.  Views of the current version
+// that someone else still holds (a copied state) are downloaded first, since
+// the mirror is about to move on.
+std::shared_ptr<Mirror> mirror_for_update(KeyCacheState& ks, ValueCacheState& vs,
+                                          const CacheConfig& cfg) {
+    std::shared_ptr<Mirror> m = current_mirror(ks, vs, cfg);
+    if (!m) return import_states(ks, vs, cfg);
+    for (auto* w : {&m->kview, &m->vview}) {
+        std::shared_ptr<DeviceView> v = w->lock();
+        // holders: this lock + the caller's state; more = an outside copy
+        if (v && v.use_count() > 2) v->fetch();
+    }
+    return m;
+}
+
+// Host copy of the reference's residual update (kv_cache.cpp:66-98) for one
+// appended token; the device does the same on its rings.
+void advance_residuals(Mirror& m, const Matrix& t_K, const Matrix& t_V) {
+    const Index R = m.cfg.residual_length, d = m.cfg.head_dim;
+    const std::size_t row = sizeof(float) * (std::size_t)d;
+    const Index kr = m.kres.rows();
+    if (kr + 1 == R) {
+        m.kres = Matrix(0, d);  // flushed into the grouped store
+    } else {
+        Matrix k(kr + 1, d);
+        if (kr) std::memcpy(k.data(), m.kres.data(), row * kr);
+        std::memcpy(k.data() + kr * d, t_K.data(), row);
+        m.kres = std::move(k);
+    }
+    const Index vr = m.vres.rows();
+    const Index keep = vr == R ? R - 1 : vr;  // the oldest row is quantized out when full
+    Matrix v(keep + 1, d);
+    if (keep) std::memcpy(v.data(), m.vres.data() + (vr - keep) * d, row * keep);
+    std::memcpy(v.data() + keep * d, t_V.data(), row);
+    m.vres = std::move(v);
 }
 
 void check_rows(const Matrix& t_K, const Matrix& t_V, const CacheConfig& cfg) {
@@ -232,20 +433,60 @@ void QuantParams::validate() const {
         throw ConfigError("group_size must be >= 1, got " + std::to_string(group_size));
 }
 
+namespace {
+// Mapped pinned staging (zero-copy: the kernel reads its inputs from and
+// writes its results to host memory over PCIe): a single-group call is one
+// kernel launch and one stream sync, ~10 us instead of three copies.
+struct Mapped {
+    std::uint8_t* p = nullptr;
+    std::size_t cap = 0;
+    std::uint8_t* get(std::size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            std::size_t want = 1 << 16;
+            while (want < bytes) want <<= 1;
+            cuda(cudaHostAlloc(reinterpret_cast<void**>(&p), want, cudaHostAllocMapped),
+                 "cudaHostAlloc");
+            cap = want;
+        }
+        return p;
+    }
+    template <typename T>
+    T* dev(T* host) {
+        void* d = nullptr;
+        cuda(cudaHostGetDevicePointer(&d, host, 0), "cudaHostGetDevicePointer");
+        return static_cast<T*>(d);
+    }
+    ~Mapped() {
+        if (p) cudaFreeHost(p);
+    }
+};
+Mapped& mapped() {
+    thread_local Mapped m;
+    return m;
+}
+std::size_t align8(std::size_t x) { return (x + 7) & ~std::size_t(7); }
+}  // namespace
+
 GroupQuant quantize_group(std::span<const float> values, int bits) {
     if (values.empty()) throw UsageError("quantize_group: empty group");
     if (bits < 1 || bits > 8) throw UsageError("quantize_group: bits out of range");
     const std::size_t n = values.size();
-    DBuf<float> m(values.data(), n);
-    DBuf<std::uint8_t> codes(n);
-    DBuf<double> z(1), s(1);
-    check(kivi_quantize_codes(m.get(), 1, (int64_t)n, bits, (int64_t)n, KIVI_PER_TOKEN,
-                              codes.get(), z.get(), s.get(), nullptr));
-    sync();
+    const std::size_t o_codes = align8(n * sizeof(float)), o_z = align8(o_codes + n);
+    std::uint8_t* buf = mapped().get(o_z + 16);
+    std::memcpy(buf, values.data(), n * sizeof(float));
+    float* din = mapped().dev(reinterpret_cast<float*>(buf));
+    std::uint8_t* dbuf = reinterpret_cast<std::uint8_t*>(din);
+    check(kivi_quantize_codes(din, 1, (int64_t)n, bits, (int64_t)n, KIVI_PER_TOKEN,
+                              dbuf + o_codes, reinterpret_cast<double*>(dbuf + o_z),
+                              reinterpret_cast<double*>(dbuf + o_z + 8), facade_stream()));
+    cuda(cudaStreamSynchronize(facade_stream()), "sync");
     GroupQuant g;
-    g.codes = codes.download(n);
-    g.zero_point = z.download(1)[0];
-    g.scale = s.download(1)[0];
+    g.codes.assign(buf + o_codes, buf + o_codes + n);
+    std::memcpy(&g.zero_point, buf + o_z, 8);
+    std::memcpy(&g.scale, buf + o_z + 8, 8);
     return g;
 }
 
@@ -253,13 +494,20 @@ std::vector<float> dequantize_group(std::span<const std::uint8_t> codes, double 
                                     double scale) {
     const std::size_t n = codes.size();
     if (n == 0) return {};
-    DBuf<std::uint8_t> c(codes.data(), n);
-    DBuf<double> z(&zero_point, 1), s(&scale, 1);
-    DBuf<float> out(n);
-    check(kivi_dequantize_codes(c.get(), z.get(), s.get(), 1, (int64_t)n, (int64_t)n,
-                                KIVI_PER_TOKEN, out.get(), nullptr));
-    sync();
-    return out.download(n);
+    const std::size_t o_z = align8(n), o_out = o_z + 16;
+    std::uint8_t* buf = mapped().get(o_out + n * sizeof(float));
+    std::memcpy(buf, codes.data(), n);
+    std::memcpy(buf + o_z, &zero_point, 8);
+    std::memcpy(buf + o_z + 8, &scale, 8);
+    std::uint8_t* dbuf = mapped().dev(buf);
+    check(kivi_dequantize_codes(dbuf, reinterpret_cast<double*>(dbuf + o_z),
+                                reinterpret_cast<double*>(dbuf + o_z + 8), 1, (int64_t)n,
+                                (int64_t)n, KIVI_PER_TOKEN, reinterpret_cast<float*>(dbuf + o_out),
+                                facade_stream()));
+    cuda(cudaStreamSynchronize(facade_stream()), "sync");
+    std::vector<float> out(n);
+    std::memcpy(out.data(), buf + o_out, n * sizeof(float));
+    return out;
 }
 
 std::vector<std::uint8_t> pack_codes(std::span<const std::uint8_t> codes, int bits) {
@@ -322,9 +570,9 @@ QuantizedTensor QuantizedTensor::quantize(const Matrix& m, const QuantParams& pa
 
 Matrix QuantizedTensor::dequantize() const {
     if (rows_ == 0) return Matrix(0, cols_);
-    const std::size_t n = (std::size_t)code_count(), ng = scales_.size();
-    DBuf<std::uint8_t> p(packed_.data(), packed_.size());
-    DBuf<double> z(zero_points_.data(), ng), s(scales_.data(), ng);
+    const std::size_t n = (std::size_t)code_count(), ng = (std::size_t)group_count();
+    DBuf<std::uint8_t> p(packed().data(), packed().size());
+    DBuf<double> z(zero_points().data(), ng), s(scales().data(), ng);
     DBuf<float> out(n);
     check(kivi_dequantize_matrix(p.get(), z.get(), s.get(), rows_, cols_, params_.bits,
                                  params_.group_size, axis_of(params_.axis), out.get(), nullptr));
@@ -339,6 +587,8 @@ void QuantizedTensor::concat_tokens(const QuantizedTensor& other) {
         *this = other;
         return;
     }
+    detail::TensorAccess::own(*this);  // host-side mutation: a device view becomes host data
+    const std::vector<std::uint8_t>& opacked = other.packed();
     if (cols_ != other.cols_)
         throw ShapeError("concat_tokens: column counts differ (" + std::to_string(cols_) + " vs " +
                          std::to_string(other.cols_) + ")");
@@ -348,15 +598,15 @@ void QuantizedTensor::concat_tokens(const QuantizedTensor& other) {
     // Device unpack of both streams + one repack (the reference's algorithm,
     // quantize.cpp:206-213).
     const std::size_t na = (std::size_t)code_count(), nb = (std::size_t)other.code_count();
-    DBuf<std::uint8_t> a(packed_.data(), packed_.size()), b(other.packed_.data(), other.packed_.size());
+    DBuf<std::uint8_t> a(packed_.data(), packed_.size()), b(opacked.data(), opacked.size());
     DBuf<std::uint8_t> codes(na + nb);
     check(kivi_unpack_codes(a.get(), (int64_t)na, params_.bits, codes.get(), nullptr));
     check(kivi_unpack_codes(b.get(), (int64_t)nb, params_.bits, codes.get() + na, nullptr));
     DBuf<std::uint8_t> out(packed_size(na + nb, params_.bits));
     check(kivi_pack_codes(codes.get(), (int64_t)(na + nb), params_.bits, out.get(), nullptr));
     packed_ = out.download(packed_size(na + nb, params_.bits));
-    zero_points_.insert(zero_points_.end(), other.zero_points_.begin(), other.zero_points_.end());
-    scales_.insert(scales_.end(), other.scales_.begin(), other.scales_.end());
+    zero_points_.insert(zero_points_.end(), other.zero_points().begin(), other.zero_points().end());
+    scales_.insert(scales_.end(), other.scales().begin(), other.scales().end());
     rows_ += other.rows_;
 }
 
@@ -402,10 +652,14 @@ PrefillResult prefill(const Matrix& keys, const Matrix& values, const CacheConfi
     if (keys.rows() != values.rows()) throw ShapeError("prefill: key/value token counts differ");
     if (keys.cols() != cfg.head_dim || values.cols() != cfg.head_dim)
         throw ShapeError("prefill: head_dim mismatch");
-    kivi_cache* h = pooled_cache(cfg);
-    check(kivi_prefill_host(h, keys.data(), values.data(), keys.rows(), nullptr));
+    const Index l = keys.rows(), R = cfg.residual_length;
+    auto m = new_mirror(cfg, l + R);
+    check(kivi_prefill_host(m->h, keys.data(), values.data(), l, facade_stream()));
+    // residual rows (kv_cache.cpp:37-49): the last l % R keys, the last min(l, R) values
+    m->kres = keys.bottomRows(l % R);
+    m->vres = values.bottomRows(std::min(l, R));
     PrefillResult out;
-    store_state(h, out.key, out.value, cfg);
+    publish(m, out.key, out.value);
     out.passthrough_keys = keys;
     out.passthrough_values = values;
     return out;
@@ -414,11 +668,19 @@ PrefillResult prefill(const Matrix& keys, const Matrix& values, const CacheConfi
 void append_token(KeyCacheState& key_state, ValueCacheState& value_state, const Matrix& t_K,
                   const Matrix& t_V, const CacheConfig& cfg) {
     check_rows(t_K, t_V, cfg);
-    kivi_cache* h = pooled_cache(cfg);
-    load_state(h, key_state, value_state, cfg);
-    check(kivi_append_host(h, t_K.data(), t_V.data(), nullptr));
-    sync();
-    store_state(h, key_state, value_state, cfg);
+    std::shared_ptr<Mirror> m = mirror_for_update(key_state, value_state, cfg);
+    const Index d = cfg.head_dim;
+    float* st = pinned(0).get(2 * d);
+    std::memcpy(st, t_K.data(), sizeof(float) * d);
+    std::memcpy(st + d, t_V.data(), sizeof(float) * d);
+    {
+        std::lock_guard<std::mutex> lk(m->mu);
+        check(kivi_append_host(m->h, st, st + d, facade_stream()));
+        cuda(cudaStreamSynchronize(facade_stream()), "sync");
+        m->version++;
+    }
+    advance_residuals(*m, t_K, t_V);
+    publish(m, key_state, value_state);
 }
 
 Matrix materialize_keys(const KeyCacheState& state) {
@@ -430,8 +692,10 @@ Matrix materialize_values(const ValueCacheState& state) {
 }
 
 namespace {
+// packed bytes from the shape (no download of a device-resident store)
 std::uint64_t grouped_bytes(const QuantizedTensor& t) {
-    return (std::uint64_t)t.packed().size() + 4u * (std::uint64_t)t.group_count();
+    return (std::uint64_t)packed_size(t.code_count(), t.params().bits) +
+           4u * (std::uint64_t)t.group_count();
 }
 }  // namespace
 
@@ -474,17 +738,30 @@ DecodeOutput decode_attention(const Matrix& t_Q, const Matrix& t_K, const Matrix
     if (t_Q.rows() != 1 || t_Q.cols() != cfg.head_dim)
         throw ShapeError("decode_attention: query must be 1x" + std::to_string(cfg.head_dim));
     check_rows(t_K, t_V, cfg);
-    kivi_cache* h = pooled_cache(cfg);
-    load_state(h, key_state, value_state, cfg);
+    std::shared_ptr<Mirror> m = mirror_for_update(key_state, value_state, cfg);
+    const Index d = cfg.head_dim;
     const Index l = key_state.total_tokens + 1;
+    float* in = pinned(0).get(3 * d);
+    std::memcpy(in, t_Q.data(), sizeof(float) * d);
+    std::memcpy(in + d, t_K.data(), sizeof(float) * d);
+    std::memcpy(in + 2 * d, t_V.data(), sizeof(float) * d);
+    float* res = pinned(1).get(d + l);
+    {
+        std::lock_guard<std::mutex> lk(m->mu);
+        cudaStream_t st = facade_stream();
+        check(kivi_decode_host(m->h, in, in + d, in + 2 * d, 1, res, res + d,
+                               opts.scale_logits ? 1 : 0, st));
+        check(kivi_host_join(m->h, st));
+        cuda(cudaStreamSynchronize(st), "sync");
+        m->version++;
+    }
     DecodeOutput out;
-    out.output = Matrix(1, cfg.head_dim);
+    out.output = Matrix(1, d);
     out.weights = Matrix(1, l);
-    check(kivi_decode_host(h, t_Q.data(), t_K.data(), t_V.data(), 1, out.output.data(),
-                           out.weights.data(), opts.scale_logits ? 1 : 0, nullptr));
-    check(kivi_host_join(h, nullptr));
-    sync();
-    store_state(h, key_state, value_state, cfg);
+    std::memcpy(out.output.data(), res, sizeof(float) * d);
+    std::memcpy(out.weights.data(), res + d, sizeof(float) * l);
+    advance_residuals(*m, t_K, t_V);
+    publish(m, key_state, value_state);
     return out;
 }
 

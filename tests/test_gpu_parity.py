@@ -572,3 +572,54 @@ def test_export_cache_unit_kvqd(cuda, tmp_path):
     if Ref.available():
         back, err = Ref().read_dump(kp)
         assert err is None and back[0].tobytes() == gk.tobytes()
+
+
+@pytest.mark.parametrize("graph", ["0", "1"])
+@pytest.mark.parametrize("qpk,U,l0", [(1, 3, 700), (1, 64, 2300), (4, 4, 900)])
+def test_decode_layers_equals_per_layer(cuda, graph, qpk, U, l0, monkeypatch):
+    """kivi_decode_layers / kivi_decode_layers_host (one call per model step,
+    optionally replayed as a CUDA graph) give bit-identical outputs and states
+    to per-layer kivi_decode calls, across a key flush."""
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", "1")
+    monkeypatch.setenv("KIVI_STEP_GRAPH", graph)
+    rng = np.random.default_rng(60 + U + qpk)
+    L, d = 3, 128
+    cfg = kb.CacheConfig(2, 32, 128, d)
+    mk = []
+    for _ in range(3):
+        cs = []
+        for ly in range(L):
+            K = rnd(np.random.default_rng(ly), U, l0, d)
+            c = kb.KVCache(cfg, U)
+            c.prefill(dev(K), dev(K * 0.5))
+            cs.append(c)
+        mk.append(cs)
+    ref, devs, host = mk
+    sd, sh = kb.LayerStack(devs), kb.LayerStack(host)
+    stream = torch.cuda.Stream()
+    hq = torch.empty((L, U, qpk, d), pin_memory=True)
+    hk = torch.empty((L, U, d), pin_memory=True)
+    hv = torch.empty((L, U, d), pin_memory=True)
+    ho = torch.empty((L, U, qpk, d), pin_memory=True)
+    for step in range(l0 % 128 and 130 - l0 % 128 or 3):
+        q, tk, tv = rnd(rng, L, U, qpk, d), rnd(rng, L, U, d), rnd(rng, L, U, d)
+        want = np.stack([ref[ly].decode(dev(q[ly]), dev(tk[ly]), dev(tv[ly]), q_per_kv=qpk)
+                         .cpu().numpy() for ly in range(L)])
+        od = torch.empty((L, U, qpk, d), device="cuda")
+        sd.decode(dev(q), dev(tk), dev(tv), od, q_per_kv=qpk)
+        hq.copy_(torch.from_numpy(q))
+        hk.copy_(torch.from_numpy(tk))
+        hv.copy_(torch.from_numpy(tv))
+        with torch.cuda.stream(stream):
+            sh.decode_host(hq, hk, hv, ho, q_per_kv=qpk, stream=stream)
+        assert od.cpu().numpy().tobytes() == want.tobytes(), step
+        assert ho.numpy().tobytes() == want.tobytes(), step
+    torch.cuda.synchronize()
+    if graph == "1":
+        stats = kb.step_graph_stats()
+        assert stats["capture_failed"] == 0 and stats["replayed"] > 0, stats
+    for ly in range(L):
+        for u in (0, U - 1):
+            a, b, c = ref[ly].export_unit(u), devs[ly].export_unit(u), host[ly].export_unit(u)
+            for key in a:
+                assert a[key].tobytes() == b[key].tobytes() == c[key].tobytes(), (ly, u, key)
