@@ -10,10 +10,9 @@
 //     D[m][n] = sum_k Wt[m][k] * x[n][k]        (Wt = W^T, prepared once)
 // fp32 accuracy from TF32 tensor cores with the 3xTF32 split
 //     x*w ~= x_hi*w_hi + x_hi*w_lo + x_lo*w_hi
-// where x_hi is x itself (the tensor core reads the top 19 bits of a tf32
-// operand, i.e. truncates) and x_lo = x - trunc_tf32(x), exact in fp32 and
-// computed in shared memory by the epilogue warps while the TMA streams the
-// next tiles.  The three products accumulate in one fp32 TMEM accumulator.
+// where x_hi = x rounded to tf32 and x_lo = the rounded remainder, computed
+// in shared memory (in place over the TMA'd tile) by the epilogue warps while
+// the TMA streams the next tiles.  The three products accumulate in one fp32 TMEM accumulator.
 //
 // Warp roles (one CTA per 128-channel tile of q, k or v, 6 warps):
 //   warp 0, one lane : TMA producer (Wt tile 128 x 32 fp32, x tile N x 32),
@@ -52,6 +51,7 @@ struct ProjArgs {
     int tiles_m;     // 128-channel tiles per matrix (hidden_out / 128)
     int stages;
     int mode;        // 0: store rows  1: decode append (k, v) + q store  2: store per unit
+    int split_mode;  // hi/lo split (see the split warps)
     // mode 0: out[which] is [rows][hidden_out] row-major
     // mode 1: out[0] = q rows [n * heads + h][128]; k / v go into the cache
     // mode 2: row = b * seq + t -> out[which][((b * heads + h) * seq + t)][128]
@@ -132,13 +132,30 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// x - trunc_tf32(x): exact in fp32 (the tensor core truncates the operand to
-// 19 bits, so x itself is the hi part).
-__device__ __forceinline__ float lo_part(float x) {
-    return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// Round-to-nearest tf32 split x = hi + lo: hi = x rounded to 10 mantissa
+// bits (what the tensor core reads of it exactly), lo = x - hi (exact in fp32,
+// |lo| <= 2^-11 |x|) rounded the same way.  The three products hi*hi, hi*lo,
+// lo*hi then carry x*w to ~2^-22 relative (the dropped lo*lo is < 2^-22);
+// with a truncating split (hi = x as the tensor core truncates it) both the
+// lo operand's own truncation and lo*lo were ~2^-20, several times the error
+// of an fp32 SIMT product.
+__device__ __forceinline__ float rn_tf32(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float trunc_tf32(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float4 trunc4(float4 x) {
+    return make_float4(trunc_tf32(x.x), trunc_tf32(x.y), trunc_tf32(x.z), trunc_tf32(x.w));
 }
 __device__ __forceinline__ float4 lo_part4(float4 x) {
-    return make_float4(lo_part(x.x), lo_part(x.y), lo_part(x.z), lo_part(x.w));
+    return make_float4(x.x - trunc_tf32(x.x), x.y - trunc_tf32(x.y), x.z - trunc_tf32(x.z),
+                       x.w - trunc_tf32(x.w));
+}
+__device__ __forceinline__ void split_tf32(float4& x, float4& lo) {
+    float4 h = make_float4(rn_tf32(x.x), rn_tf32(x.y), rn_tf32(x.z), rn_tf32(x.w));
+    lo = make_float4(rn_tf32(x.x - h.x), rn_tf32(x.y - h.y), rn_tf32(x.z - h.z), rn_tf32(x.w - h.w));
+    x = h;
 }
 
 // The value FIFO pop for one 32-channel group held one channel per lane: the
@@ -202,8 +219,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(tmem_full, 1);
         fence_mbar_init();
     }
-    uint32_t ncols = 32;
-    while ((int)ncols < N) ncols <<= 1;
+    // Accumulator chunks: the tensor core's fp32 accumulation rounds once per
+    // MMA against the running sum, so its error grows with the number of MMAs
+    // folded into one accumulator (measured: 1.3e-6 relative at K = 128,
+    // 3e-5 at K = 4096).  K is split over up to 8 accumulators in TMEM (as
+    // many as 512 columns hold) that the epilogue adds in fp32.
+    uint32_t ncols_per = 32;
+    while ((int)ncols_per < N) ncols_per <<= 1;
+    int nchunk = 1;
+    while (nchunk < 8 && (uint32_t)(2 * nchunk) * ncols_per <= 512u && 2 * nchunk <= nkb) nchunk <<= 1;
+    const uint32_t ncols = (uint32_t)nchunk * ncols_per;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -234,6 +259,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t idesc = tf32_idesc(N);
             for (int kb = 0; kb < nkb; ++kb) {
                 const int s = kb % S;
+                const int chunk = kb * nchunk / nkb;
+                const bool first = kb == (chunk * nkb + nchunk - 1) / nchunk;  // chunk's first kb
+                const uint32_t acc = tmem + (uint32_t)chunk * ncols_per;
                 mbar_wait(&split[s], (kb / S) & 1);
                 tc_fence_after();
                 const uint32_t st = smem_u32(base + s * stage_bytes);
@@ -244,9 +272,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const uint32_t off = kk * UK * 4;  // 32 bytes per K step inside the atom
                     const uint64_t da = sw128_desc(sa + off), dal = sw128_desc(sa_lo + off);
                     const uint64_t db = sw128_desc(sb + off), dbl = sw128_desc(sb_lo + off);
-                    mma_tf32(tmem, da, db, idesc, (kb | kk) != 0);
-                    mma_tf32(tmem, da, dbl, idesc, 1);
-                    mma_tf32(tmem, dal, db, idesc, 1);
+                    mma_tf32(acc, da, db, idesc, !(first && kk == 0));
+                    mma_tf32(acc, da, dbl, idesc, 1);
+                    mma_tf32(acc, dal, db, idesc, 1);
                 }
                 umma_commit(&empty[s]);  // the stage is free once these MMAs completed
             }
@@ -259,14 +287,42 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int s = kb % S;
             mbar_wait(&full[s], (kb / S) & 1);
             uint8_t* st = base + s * stage_bytes;
-            const float4* A = reinterpret_cast<const float4*>(st);
+            float4* A = reinterpret_cast<float4*>(st);
             float4* Alo = reinterpret_cast<float4*>(st + a_bytes);
-            const float4* Bx = reinterpret_cast<const float4*>(st + 2 * a_bytes);
+            float4* Bx = reinterpret_cast<float4*>(st + 2 * a_bytes);
             float4* Blo = reinterpret_cast<float4*>(st + 2 * a_bytes + b_bytes);
-            // same byte offsets: the lo tiles inherit the TMA's swizzled layout
+            // split_mode 0: hi = the TMA'd tile itself (the tensor core
+            // truncates it), lo = x - trunc(x); 1: hi = trunc(x) written in
+            // place; 2: round-to-nearest hi and lo (split_tf32)
+            if (a.split_mode == 0) {
 #pragma unroll 4
-            for (int i = t; i < (int)(a_bytes / 16); i += 128) Alo[i] = lo_part4(A[i]);
-            for (int i = t; i < (int)(b_bytes / 16); i += 128) Blo[i] = lo_part4(Bx[i]);
+                for (int i = t; i < (int)(a_bytes / 16); i += 128) Alo[i] = lo_part4(A[i]);
+                for (int i = t; i < (int)(b_bytes / 16); i += 128) Blo[i] = lo_part4(Bx[i]);
+            } else if (a.split_mode == 1) {
+                for (int i = t; i < (int)(a_bytes / 16); i += 128) {
+                    const float4 x = A[i];
+                    Alo[i] = lo_part4(x);
+                    A[i] = trunc4(x);
+                }
+                for (int i = t; i < (int)(b_bytes / 16); i += 128) {
+                    const float4 x = Bx[i];
+                    Blo[i] = lo_part4(x);
+                    Bx[i] = trunc4(x);
+                }
+            } else {
+                for (int i = t; i < (int)(a_bytes / 16); i += 128) {
+                    float4 x = A[i], lo;
+                    split_tf32(x, lo);
+                    A[i] = x;
+                    Alo[i] = lo;
+                }
+                for (int i = t; i < (int)(b_bytes / 16); i += 128) {
+                    float4 x = Bx[i], lo;
+                    split_tf32(x, lo);
+                    Bx[i] = x;
+                    Blo[i] = lo;
+                }
+            }
             fence_proxy_async_smem();  // generic-proxy writes -> tensor-core (async) reads
             mbar_arrive(&split[s]);
         }
@@ -279,6 +335,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c0 = 0; c0 < N; c0 += 16) {
             float v[16];
             tmem_ld16(taddr + c0, v);
+            for (int ch = 1; ch < nchunk; ++ch) {
+                float w[16];
+                tmem_ld16(taddr + (uint32_t)ch * ncols_per + c0, w);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] += w[j];
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int n = c0 + j;

@@ -322,7 +322,7 @@ int env_int(const char* name, int dflt) {
 struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
-    int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph;
+    int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -342,6 +342,8 @@ struct Tuning {
         gqa_partial = env_int("KIVI_GQA_PARTIAL", 1);
         gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
         step_graph = env_int("KIVI_STEP_GRAPH", 0);
+        zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
+        proj_split = env_int("KIVI_PROJ_SPLIT", 2);
     }
 };
 Tuning g_tune;
@@ -1494,6 +1496,18 @@ struct StepStage {
         if (exec) cudaGraphExecDestroy(exec);
     }
 };
+// Device address of pinned, device-mapped host memory (cudaHostAlloc /
+// cudaHostRegister; with unified addressing every pinned allocation is
+// mapped), or nullptr for pageable memory.
+const float* mapped(const float* host) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+    return static_cast<const float*>(at.devicePointer);
+}
 StepStage& step_stage() {
     thread_local StepStage s[kMaxDevices];
     int dev = 0;
@@ -1529,17 +1543,33 @@ kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers,
     KIVI_CUDA(sg.init(n_layers));
     cudaStream_t st = S(stream);
     const int64_t qrow = U * q_per_kv * d, krow = U * d;
+    // zero-copy rows (one layer, rows <= KIVI_ZERO_COPY_BYTES, default 64 KiB)
+    const bool zero_copy =
+        n_layers == 1 && (int64_t)sizeof(float) * qrow <= tune().zero_copy_bytes;
     auto enqueue = [&]() -> kivi_status {
         if (n_layers == 1) {
             // one layer: nothing to overlap the copies with; one stream
-            // avoids the cross-stream event latencies (C1: a ~25 us step)
+            // avoids the cross-stream event latencies (C1: a ~25 us step).
+            // Small rows in pinned (device-mapped) host memory skip the copy
+            // engine: the append kernel reads the key/value rows and the
+            // merge kernel writes the outputs across PCIe itself (each copy
+            // is a few us of DMA setup on a latency-bound step).  q is read
+            // by every item of the attend, so it is uploaded.
+            const float* dk = zero_copy ? mapped(t_k) : nullptr;
+            const float* dv = zero_copy ? mapped(t_v) : nullptr;
+            float* dout = zero_copy ? const_cast<float*>(mapped(out)) : nullptr;
             KIVI_CUDA(cudaMemcpyAsync(sg.q, t_q, sizeof(float) * qrow, cudaMemcpyHostToDevice, st));
-            KIVI_CUDA(cudaMemcpyAsync(sg.k, t_k, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
-            KIVI_CUDA(cudaMemcpyAsync(sg.v, t_v, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
-            kivi_status r = kivi_decode(caches[0], sg.q, sg.k, sg.v, q_per_kv, sg.out, nullptr,
-                                        scale_logits, stream);
+            if (!dk || !dv) {
+                KIVI_CUDA(cudaMemcpyAsync(sg.k, t_k, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
+                KIVI_CUDA(cudaMemcpyAsync(sg.v, t_v, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
+                dk = sg.k;
+                dv = sg.v;
+            }
+            kivi_status r = kivi_decode(caches[0], sg.q, dk, dv, q_per_kv, dout ? dout : sg.out,
+                                        nullptr, scale_logits, stream);
             if (r) return r;
-            KIVI_CUDA(cudaMemcpyAsync(out, sg.out, sizeof(float) * qrow, cudaMemcpyDeviceToHost, st));
+            if (!dout)
+                KIVI_CUDA(cudaMemcpyAsync(out, sg.out, sizeof(float) * qrow, cudaMemcpyDeviceToHost, st));
             return KIVI_OK;
         }
         // fork the copy streams off `stream` (this call's work starts after
@@ -1759,6 +1789,7 @@ kivi_status launch_proj(kivi_proj* p, const float* x, int64_t n, proj::ProjArgs 
     a.tiles_m = (int)(p->hidden_out / proj::BM);
     a.stages = std::max(2, std::min(std::min(6, nkb), proj::SMEM_LIMIT / stage));
     a.hidden_out = (int)p->hidden_out;
+    a.split_mode = tune().proj_split;
     const size_t smem = 1024 + (size_t)a.stages * stage + (3 * a.stages + 2) * 8;
     auto kern = bits == 4 ? proj::proj_kernel<4> : proj::proj_kernel<2>;
     KIVI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -439,11 +440,13 @@ namespace {
 // kernel launch and one stream sync, ~10 us instead of three copies.
 struct Mapped {
     std::uint8_t* p = nullptr;
+    std::uint8_t* dbase = nullptr;  // device address of p (cached per allocation)
     std::size_t cap = 0;
     std::uint8_t* get(std::size_t bytes) {
         if (bytes > cap) {
             if (p) cudaFreeHost(p);
             p = nullptr;
+            dbase = nullptr;
             cap = 0;
             std::size_t want = 1 << 16;
             while (want < bytes) want <<= 1;
@@ -455,9 +458,12 @@ struct Mapped {
     }
     template <typename T>
     T* dev(T* host) {
-        void* d = nullptr;
-        cuda(cudaHostGetDevicePointer(&d, host, 0), "cudaHostGetDevicePointer");
-        return static_cast<T*>(d);
+        if (!dbase) {
+            void* d = nullptr;
+            cuda(cudaHostGetDevicePointer(&d, p, 0), "cudaHostGetDevicePointer");
+            dbase = static_cast<std::uint8_t*>(d);
+        }
+        return reinterpret_cast<T*>(dbase + (reinterpret_cast<std::uint8_t*>(host) - p));
     }
     ~Mapped() {
         if (p) cudaFreeHost(p);
@@ -466,6 +472,69 @@ struct Mapped {
 Mapped& mapped() {
     thread_local Mapped m;
     return m;
+}
+
+// Completion of the facade stream's work as seen from the host, for the
+// single-group round trips (quantize_group / dequantize_group): a stream
+// memory operation (cuStreamWriteValue32, with its implied system-scope
+// fence) writes a sequence number into mapped host memory once the kernel has
+// finished, and the host spins on it -- ~4 us less per call than
+// cudaStreamSynchronize, which the reference's acceptance criterion 1
+// (3x10^5 quantize + dequantize round trips within 10 s) needs.  Falls back
+// to cudaStreamSynchronize where stream memory operations are unavailable.
+typedef int (*StreamWriteValue32Fn)(void* stream, unsigned long long addr, unsigned int value,
+                                    unsigned int flags);
+struct Waiter {
+    volatile std::uint32_t* hflag = nullptr;
+    unsigned long long dflag = 0;
+    std::uint32_t seq = 0;
+    StreamWriteValue32Fn fn = nullptr;
+    bool usable = false;
+    Waiter() {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return;
+        void* h = nullptr;
+        if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) != cudaSuccess) return;
+        void* d = nullptr;
+        if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+            cudaFreeHost(h);
+            return;
+        }
+        hflag = static_cast<volatile std::uint32_t*>(h);
+        *hflag = 0;
+        dflag = reinterpret_cast<unsigned long long>(d);
+        fn = reinterpret_cast<StreamWriteValue32Fn>(f);
+        usable = true;
+    }
+    ~Waiter() {
+        if (hflag) cudaFreeHost(const_cast<std::uint32_t*>(hflag));
+    }
+    void wait(cudaStream_t st) {
+        if (usable) {
+            const std::uint32_t want = ++seq;
+            if (fn(st, dflag, want, 0) == 0) {
+                for (std::uint64_t spin = 1; *hflag != want; ++spin) {
+                    if ((spin & 0xFFFF) == 0) {  // a failed kernel never signals
+                        const cudaError_t e = cudaStreamQuery(st);
+                        if (e != cudaSuccess && e != cudaErrorNotReady) cuda(e, "stream");
+                        if (e == cudaSuccess && *hflag != want) break;
+                    }
+                }
+                std::atomic_thread_fence(std::memory_order_acquire);
+                if (*hflag == want) return;
+            } else {
+                usable = false;
+            }
+        }
+        cuda(cudaStreamSynchronize(st), "sync");
+    }
+};
+void facade_wait(cudaStream_t st) {
+    thread_local Waiter w;
+    w.wait(st);
 }
 std::size_t align8(std::size_t x) { return (x + 7) & ~std::size_t(7); }
 }  // namespace
@@ -482,7 +551,7 @@ GroupQuant quantize_group(std::span<const float> values, int bits) {
     check(kivi_quantize_codes(din, 1, (int64_t)n, bits, (int64_t)n, KIVI_PER_TOKEN,
                               dbuf + o_codes, reinterpret_cast<double*>(dbuf + o_z),
                               reinterpret_cast<double*>(dbuf + o_z + 8), facade_stream()));
-    cuda(cudaStreamSynchronize(facade_stream()), "sync");
+    facade_wait(facade_stream());
     GroupQuant g;
     g.codes.assign(buf + o_codes, buf + o_codes + n);
     std::memcpy(&g.zero_point, buf + o_z, 8);
@@ -504,7 +573,7 @@ std::vector<float> dequantize_group(std::span<const std::uint8_t> codes, double 
                                 reinterpret_cast<double*>(dbuf + o_z + 8), 1, (int64_t)n,
                                 (int64_t)n, KIVI_PER_TOKEN, reinterpret_cast<float*>(dbuf + o_out),
                                 facade_stream()));
-    cuda(cudaStreamSynchronize(facade_stream()), "sync");
+    facade_wait(facade_stream());
     std::vector<float> out(n);
     std::memcpy(out.data(), buf + o_out, n * sizeof(float));
     return out;

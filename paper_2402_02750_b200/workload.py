@@ -8,10 +8,14 @@ Mirrors reference proj/include/kivi/workload.hpp / src/workload.cpp:
     decode steps over synthetic projections, one cache per (batch, layer, head)
 
 run_decode_benchmark is the reference's only in-tree caller of the hot path.  Here it
-drives the B200 library the way a serving loop would: per layer, ONE batched GEMM
-projects every sequence's token (t @ W_q/k/v, cuBLAS fp32 — a plain library GEMM, as the
-reference's Eigen matmul, workload.cpp:230-232) straight into the [units][d] rows the
-decode kernels take (unit = batch * kv_heads + head), then one kivi_decode per layer.
+drives the B200 library the way a serving loop would.  Per layer and step, ONE launch
+(kivi_proj_append, tcgen05 3xTF32 tensor cores) projects every sequence's token
+(t @ W_q/k/v, workload.cpp:230-232) and appends the new key/value rows straight into the
+caches (unit = batch * kv_heads + head) -- the value FIFO pop is quantized in the GEMM
+epilogue -- then one kivi_attend per layer reads the q rows it wrote.  The prompt's
+projections use the same kernel (kivi_proj_gemm, per-unit output layout) before the bulk
+prefill.  Shapes the fused kernel does not cover (head_dim != 128, hidden % 32 != 0,
+group size != 32, bits not in {2, 4}) use cuBLAS fp32 GEMMs and kivi_decode.
 Peak cache bytes are counted from the live device states (kivi_cache_get_info, the
 reference's memory_bytes) and checked against the budget after prefill and every step,
 as the reference does (workload.cpp:175-192).
@@ -26,7 +30,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, replace
 
-from . import BudgetError, CacheConfig, ConfigError, KVCache, UsageError
+from . import BudgetError, CacheConfig, ConfigError, KVCache, Projection, UsageError
 
 
 @dataclass(frozen=True)
@@ -157,13 +161,16 @@ def _percentile(sorted_ms, q):  # workload.cpp:135-141
 
 def run_decode_benchmark(spec: WorkloadSpec, cfg: CacheConfig, seed: int = 0,
                          mode: str = "kivi", budget_bytes: int | None = None, data=None,
-                         device: int | None = None) -> BenchReport:
+                         device: int | None = None,
+                         fused_projection: bool | None = None) -> BenchReport:
     """Reference run_decode_benchmark (workload.cpp:145-271) on the GPU.
 
     data: optional (weights [layers, 3, hidden, hidden], prompts [batch, prompt_len, hidden],
     tokens [gen_len, batch, hidden]) fp32 arrays, e.g. the reference's own draws; by
     default they are drawn on the device from `seed` (N(0, 1), weights scaled by
     1/sqrt(hidden) as SyntheticLayer does, workload.cpp:116-122).
+    fused_projection: None = the tensor-core projection fused with the append
+    wherever its shape constraints hold; False = cuBLAS GEMMs + kivi_decode.
     """
     import torch
     spec.validate()
@@ -186,10 +193,21 @@ def run_decode_benchmark(spec: WorkloadSpec, cfg: CacheConfig, seed: int = 0,
         n = x.shape[1]
         return x.view(Bt, n, H, d).permute(0, 2, 1, 3).reshape(U, n, d).contiguous()
 
+    # the fused tensor-core projection + append (kernels_project.cuh)
+    fused = (mode == "kivi" and d == 128 and hid % 32 == 0 and cfg.group_size == 32
+             and cfg.bits in (2, 4) and cfg.head_dim == 128 and fused_projection is not False)
+    if fused_projection and not fused:
+        raise ConfigError("fused projection needs head_dim 128, hidden % 32 == 0, group 32, "
+                          "2 or 4 bits, mode 'kivi'")
+    projs = [Projection(W[ly, 0], W[ly, 1], W[ly, 2]) for ly in range(spec.layers)] \
+        if fused else []
     caches, fp = [], []
     for ly in range(spec.layers):
-        K = units(torch.matmul(P, W[ly, 1]))
-        V = units(torch.matmul(P, W[ly, 2]))
+        if fused:
+            _, K, V = projs[ly].gemm(P.reshape(Bt * spec.prompt_len, hid), seq=spec.prompt_len)
+        else:
+            K = units(torch.matmul(P, W[ly, 1]))
+            V = units(torch.matmul(P, W[ly, 2]))
         if mode == "kivi":
             c = KVCache(cfg, U, capacity_tokens=spec.total_len(), device=dev.index)
             c.prefill(K, V)
@@ -224,6 +242,11 @@ def run_decode_benchmark(spec: WorkloadSpec, cfg: CacheConfig, seed: int = 0,
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for ly in range(spec.layers):
+            if fused:
+                out = caches[ly].attend(projs[ly].append(caches[ly], t))
+                checksum += out.double().sum()
+                abs_sum += out.double().abs().sum()
+                continue
             q, k, v = (torch.matmul(t, W[ly, i]).view(U, 1, d) for i in range(3))
             if mode == "kivi":
                 out = caches[ly].decode(q, k.view(U, d), v.view(U, d))
@@ -249,4 +272,93 @@ def run_decode_benchmark(spec: WorkloadSpec, cfg: CacheConfig, seed: int = 0,
                       output_abs_sum=float(abs_sum.item()))
     for c in caches:
         c.close()
+    for p_ in projs:
+        p_.close()
     return rep
+
+
+# ---- native driver (libkivi_driver.so, include/kivi_driver.h) -----------------
+
+DRIVER_PATH = __import__("os").path.join(__import__("os").path.dirname(__file__),
+                                         "libkivi_driver.so")
+DRIVER_SYMBOLS = ("kivi_run_decode_benchmark", "kivi_driver_last_error")
+_driver = None
+
+
+def driver_lib():
+    """libkivi_driver.so: the C++ decode driver over the C-ABI (raises if not built)."""
+    import ctypes
+    global _driver
+    if _driver is None:
+        from . import lib
+        lib()  # libkivi_b200.so first (the driver links it)
+        import os
+        if not os.path.exists(DRIVER_PATH):
+            raise ImportError(f"{DRIVER_PATH} is missing: build it with "
+                              "`make -C paper_2402_02750_b200`")
+        L = ctypes.CDLL(DRIVER_PATH)
+        L.kivi_run_decode_benchmark.restype = ctypes.c_int
+        L.kivi_run_decode_benchmark.argtypes = [
+            ctypes.POINTER(_Spec), ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+            ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+            ctypes.POINTER(_Report)]
+        L.kivi_driver_last_error.restype = ctypes.c_char_p
+        L.kivi_driver_last_error.argtypes = []
+        _driver = L
+    return _driver
+
+
+import ctypes as _ct  # noqa: E402
+
+
+class _Spec(_ct.Structure):
+    _fields_ = [(n, _ct.c_int64) for n in
+                ("batch", "prompt_len", "gen_len", "layers", "kv_heads", "head_dim")]
+
+
+class _Report(_ct.Structure):
+    _fields_ = [("decode_steps", _ct.c_int64), ("tokens_per_sec", _ct.c_double),
+                ("p50_ms", _ct.c_double), ("p90_ms", _ct.c_double), ("p99_ms", _ct.c_double),
+                ("peak_cache_bytes", _ct.c_uint64), ("output_checksum", _ct.c_double),
+                ("output_abs_sum", _ct.c_double), ("decode_seconds", _ct.c_double),
+                ("n_devices", _ct.c_int32)]
+
+
+def run_decode_benchmark_native(spec: WorkloadSpec, cfg: CacheConfig, seed: int = 0,
+                                devices=(0,), data=None,
+                                budget_bytes: int | None = None) -> BenchReport:
+    """The reference's run_decode_benchmark (workload.cpp:145-271) in the C++ driver
+    (kivi_run_decode_benchmark): one host thread per entry of `devices`, the batch split
+    into contiguous blocks, fused tensor-core projection + append and one attend per
+    layer and step.  data: optional host (weights [layers, 3, hidden, hidden], prompts
+    [batch, prompt_len, hidden], tokens [gen_len, batch, hidden]) fp32 arrays; without
+    it the driver draws N(0, 1) data on the devices from `seed` (its own generator, so
+    checksums match run_decode_benchmark only for the same `data`)."""
+    import numpy as np
+    from . import _ERRORS, KiviError
+    spec.validate()
+    keep = []
+    ptrs = [None, None, None]
+    if data is not None:
+        for i, a in enumerate(data):
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+            keep.append(a)
+            ptrs[i] = a.ctypes.data
+    dev = (_ct.c_int32 * len(devices))(*devices)
+    sp = _Spec(spec.batch, spec.prompt_len, spec.gen_len, spec.layers, spec.kv_heads,
+               spec.head_dim)
+    c = cfg._c()
+    rep = _Report()
+    L = driver_lib()
+    st = L.kivi_run_decode_benchmark(_ct.byref(sp), _ct.addressof(c), dev, len(devices),
+                                     int(seed) & (2 ** 64 - 1), ptrs[0], ptrs[1], ptrs[2],
+                                     int(budget_bytes or 0), _ct.byref(rep))
+    if st != 0:
+        msg = L.kivi_driver_last_error().decode(errors="replace")
+        if st == 6 and "budget" in msg:
+            raise BudgetError(msg)
+        raise _ERRORS.get(st, KiviError)(msg)
+    return BenchReport(mode="kivi", decode_steps=rep.decode_steps,
+                       tokens_per_sec=rep.tokens_per_sec, p50_ms=rep.p50_ms, p90_ms=rep.p90_ms,
+                       p99_ms=rep.p99_ms, peak_cache_bytes=rep.peak_cache_bytes,
+                       output_checksum=rep.output_checksum, output_abs_sum=rep.output_abs_sum)

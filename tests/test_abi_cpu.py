@@ -126,3 +126,24 @@ def test_facade_library_exports_reference_api():
                 "kivi::QuantizedTensor::quantize(", "kivi::QuantizedTensor::dequantize(",
                 "kivi::QuantizedTensor::concat_tokens(", "kivi::CacheConfig::validate("):
         assert sym in syms, sym
+
+
+def test_driver_library_exports_its_header():
+    """libkivi_driver.so (the C++ decode driver) exports include/kivi_driver.h."""
+    from paper_2402_02750_b200 import workload as wl
+    declared = header_functions(os.path.join(ROOT, "include", "kivi_driver.h"))
+    assert declared == set(wl.DRIVER_SYMBOLS), declared
+    L = wl.driver_lib()
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_driver_validates_before_touching_a_device():
+    """Spec/config errors come back as the reference's exception types with no GPU."""
+    from paper_2402_02750_b200 import workload as wl
+    sp = wl.WorkloadSpec(batch=1, prompt_len=4, gen_len=1, layers=1, kv_heads=1, head_dim=64)
+    with pytest.raises(kb.ConfigError):   # fused projection needs head_dim 128
+        wl.run_decode_benchmark_native(sp, kb.CacheConfig(2, 32, 128, 64))
+    with pytest.raises(kb.ConfigError):   # workload counts must be >= 1
+        wl.run_decode_benchmark_native(wl.WorkloadSpec(batch=0, head_dim=128),
+                                       kb.CacheConfig(2, 32, 128, 128))
