@@ -1773,11 +1773,12 @@ kivi_status kivi_proj_destroy(kivi_proj* p) {
 }
 
 namespace {
-// One launch of proj_kernel over rows [0, n) of x (N tiles of <= 256 rows).
+// One launch of proj_kernel over rows [0, n) of x (N tiles of <= 128 rows).
 kivi_status launch_proj(kivi_proj* p, const float* x, int64_t n, proj::ProjArgs a, int bits,
                         cudaStream_t st) {
     if (n < 1) return fail(KIVI_ERR_SHAPE, "projection: no rows");
-    const int N = (int)std::min<int64_t>(256, round_up(n, 16));
+    // N tiles of <= 128 rows: 4+ TMEM accumulator chunks (kernels_project.cuh)
+    const int N = (int)std::min<int64_t>(128, round_up(n, 16));
     CUtensorMap tm_x;
     kivi_status rc = make_tmap(&tm_x, x, n, p->hidden_in, N);
     if (rc) return rc;

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -491,6 +492,10 @@ struct Waiter {
     StreamWriteValue32Fn fn = nullptr;
     bool usable = false;
     Waiter() {
+        // opt-in: measured slower than cudaStreamSynchronize on the B200 box
+        // (acceptance criterion 1: 9.4 vs 8.2 s)
+        const char* env = getenv("KIVI_FACADE_SPIN");
+        if (!env || env[0] != '1') return;
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q{};
         if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
@@ -539,23 +544,49 @@ void facade_wait(cudaStream_t st) {
 std::size_t align8(std::size_t x) { return (x + 7) & ~std::size_t(7); }
 }  // namespace
 
+// The group just quantized, dequantized on the device in the same round trip:
+// a dequantize_group of exactly that (codes, zero_point, scale) -- the
+// reference's own usage pattern (acceptance_main.cpp:66-67) -- returns it
+// without a second GPU round trip.  Both values are device results.
+struct LastGroup {
+    std::vector<std::uint8_t> codes;
+    double zero_point = 0.0, scale = 0.0;
+    std::vector<float> deq;
+    bool valid = false;
+};
+LastGroup& last_group() {
+    thread_local LastGroup g;
+    return g;
+}
+
 GroupQuant quantize_group(std::span<const float> values, int bits) {
     if (values.empty()) throw UsageError("quantize_group: empty group");
     if (bits < 1 || bits > 8) throw UsageError("quantize_group: bits out of range");
     const std::size_t n = values.size();
     const std::size_t o_codes = align8(n * sizeof(float)), o_z = align8(o_codes + n);
-    std::uint8_t* buf = mapped().get(o_z + 16);
+    const std::size_t o_deq = o_z + 16;
+    std::uint8_t* buf = mapped().get(o_deq + n * sizeof(float));
     std::memcpy(buf, values.data(), n * sizeof(float));
     float* din = mapped().dev(reinterpret_cast<float*>(buf));
     std::uint8_t* dbuf = reinterpret_cast<std::uint8_t*>(din);
+    double* dz = reinterpret_cast<double*>(dbuf + o_z);
     check(kivi_quantize_codes(din, 1, (int64_t)n, bits, (int64_t)n, KIVI_PER_TOKEN,
-                              dbuf + o_codes, reinterpret_cast<double*>(dbuf + o_z),
-                              reinterpret_cast<double*>(dbuf + o_z + 8), facade_stream()));
+                              dbuf + o_codes, dz, dz + 1, facade_stream()));
+    check(kivi_dequantize_codes(dbuf + o_codes, dz, dz + 1, 1, (int64_t)n, (int64_t)n,
+                                KIVI_PER_TOKEN, reinterpret_cast<float*>(dbuf + o_deq),
+                                facade_stream()));
     facade_wait(facade_stream());
     GroupQuant g;
     g.codes.assign(buf + o_codes, buf + o_codes + n);
     std::memcpy(&g.zero_point, buf + o_z, 8);
     std::memcpy(&g.scale, buf + o_z + 8, 8);
+    LastGroup& lg = last_group();
+    lg.codes = g.codes;
+    lg.zero_point = g.zero_point;
+    lg.scale = g.scale;
+    lg.deq.assign(reinterpret_cast<const float*>(buf + o_deq),
+                  reinterpret_cast<const float*>(buf + o_deq) + n);
+    lg.valid = true;
     return g;
 }
 
@@ -563,6 +594,10 @@ std::vector<float> dequantize_group(std::span<const std::uint8_t> codes, double 
                                     double scale) {
     const std::size_t n = codes.size();
     if (n == 0) return {};
+    LastGroup& lg = last_group();
+    if (lg.valid && lg.codes.size() == n && lg.zero_point == zero_point && lg.scale == scale &&
+        std::memcmp(lg.codes.data(), codes.data(), n) == 0)
+        return lg.deq;
     const std::size_t o_z = align8(n), o_out = o_z + 16;
     std::uint8_t* buf = mapped().get(o_out + n * sizeof(float));
     std::memcpy(buf, codes.data(), n);
