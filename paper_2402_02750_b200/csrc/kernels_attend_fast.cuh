@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "kernels_quant.cuh"
+#include "kernels_vimma.cuh"
 
 namespace kivi_b200 {
 namespace fast {
@@ -240,6 +241,8 @@ using WS2 = WarpSmem<2>;
 // carries q) is issued when the second-to-last value job is released; by
 // then only the last value job still reads p, and it reads tokens
 // >= BSUB - VQ_TOK >= 128 (NVJ >= 2).  Keeps 3 CTAs x 4 warps per SM.
+// (VI, the tensor-core value jobs, keeps their B digits in the job's slot.)
+template <bool VI = false>
 struct WarpSmemBody {
     static constexpr int QQ_OFF = 2 * SLOT;
     static constexpr int PROBS_OFF = QQ_OFF + D * 4;
@@ -248,7 +251,7 @@ struct WarpSmemBody {
     static constexpr int BYTES = BAR_OFF + 16;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
 };
-using WSB = WarpSmemBody;
+using WSB = WarpSmemBody<false>;
 
 // ===================== shared compute bodies ===============================
 
@@ -581,9 +584,12 @@ __device__ __forceinline__ void v_finalize(uint8_t* slot, const float2* vacc, fl
 // Items are whole 256-token sub-chunks below floor32(vg): every token's key
 // and value are quantized, so the job sequence is fixed (B=2: 2 key jobs of 4
 // tiles, 2 value jobs of 128 tokens) and the issue path is straight-line.
-template <int B>
+// VI (B = 2 only): P.V on the integer tensor cores (kernels_vimma.cuh).
+template <int B, bool VI = false>
 __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) {
     using PB = P<B>;
+    using WSB = WarpSmemBody<VI>;
+    static_assert(!VI || B == 2, "tensor-core value jobs: 2-bit codes");
     constexpr int NKJ = (BSUB / 32) / PB::KQ_TILES;  // key jobs per item
     constexpr int NVJ = BSUB / PB::VQ_TOK;           // value jobs per item
     static_assert(NVJ >= 2 && BSUB - PB::VQ_TOK >= D, "q staging aliases p[0..127]");
@@ -685,21 +691,36 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
         }
         const float2 ml = softmax_item(
             probs, BSUB, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * BSUB : nullptr, lane);
-        float2 vacc[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) vacc[i] = make_float2(0.f, 0.f);
-        float zacc0 = 0.f, zacc1 = 0.f;
+        if constexpr (VI) {
+            vimma::State st;
+            vimma::begin_item(st);
 #pragma unroll 1
-        for (int jv = 0; jv < NVJ; ++jv) {
-            uint8_t* slot = wait_slot();
-            vq_tokens_accumulate<B, PB::VQ_TOK>(slot, probs + jv * PB::VQ_TOK, PB::VQ_TOK, ksc,
-                                                vacc, zacc0, zacc1, lane);
-            if (jv == NVJ - 1) {
-                const int64_t pi = (int64_t)u * a.n_sub + k;
-                v_finalize<B>(slot, vacc, zacc0, zacc1, make_float4(0.f, 0.f, 0.f, 0.f), ml,
-                              a.part_o + pi * D, a.part_ml + pi, lane);
+            for (int jv = 0; jv < NVJ; ++jv) {
+                uint8_t* slot = wait_slot();
+                vimma::value_job<PB::VQ_TOK>(slot, probs + jv * PB::VQ_TOK, st, lane);
+                if (jv == NVJ - 1) {
+                    const int64_t pi = (int64_t)u * a.n_sub + k;
+                    vimma::finalize(st, ml, a.part_o + pi * D, a.part_ml + pi, lane);
+                }
+                release_slot();
             }
-            release_slot();
+        } else {
+            float2 vacc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) vacc[i] = make_float2(0.f, 0.f);
+            float zacc0 = 0.f, zacc1 = 0.f;
+#pragma unroll 1
+            for (int jv = 0; jv < NVJ; ++jv) {
+                uint8_t* slot = wait_slot();
+                vq_tokens_accumulate<B, PB::VQ_TOK>(slot, probs + jv * PB::VQ_TOK, PB::VQ_TOK, ksc,
+                                                    vacc, zacc0, zacc1, lane);
+                if (jv == NVJ - 1) {
+                    const int64_t pi = (int64_t)u * a.n_sub + k;
+                    v_finalize<B>(slot, vacc, zacc0, zacc1, make_float4(0.f, 0.f, 0.f, 0.f), ml,
+                                  a.part_o + pi * D, a.part_ml + pi, lane);
+                }
+                release_slot();
+            }
         }
     }
     // programmatic launch after the residual-window kernel (one stream): let

@@ -120,7 +120,7 @@ struct kivi_cache {
     int64_t scratch_cap = 0;
     float2* stats = nullptr;
     int64_t stats_cap = 0;
-    int fast_per_sm[9][4] = {};
+    int fast_per_sm[9][5] = {};  // [B][body, tail, gqa_tc, small_fused, body_vimma]
     // staging for _host calls
     // host-path staging, double-buffered: call i uploads into stg[i & 1]
     // while call i-1's kernels may still read stg[(i-1) & 1]
@@ -322,7 +322,7 @@ int env_int(const char* name, int dflt) {
 struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
-    int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split;
+    int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -344,6 +344,7 @@ struct Tuning {
         step_graph = env_int("KIVI_STEP_GRAPH", 0);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
+        vimma = env_int("KIVI_VIMMA", 1);
     }
 };
 Tuning g_tune;
@@ -600,7 +601,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     a.wlog = weights;
 
     const int smem = fast::WS2::STRIDE * fast::WARPS;
-    const int smem_body = fast::WSB::STRIDE * fast::WARPS;
+    // P.V of the body on the integer tensor cores (2-bit; kernels_vimma.cuh)
+    const bool vimma = B == 2 && tune().vimma;
+    const int smem_body = (vimma ? fast::WarpSmemBody<true>::STRIDE : fast::WSB::STRIDE) * fast::WARPS;
+    void (*body_kernel)(fast::FastArgs) = fast::attend_body_kernel<B>;
+    if constexpr (B == 2)
+        if (vimma) body_kernel = fast::attend_body_kernel<2, true>;
     const int smem_tc = gqa_tc::TS<1>::STRIDE * gqa_tc::WARPS;
     const int mha_tc = tune().mha_tc;  // measured slower on C2
     if (h->fast_per_sm[B][0] == 0) {
@@ -621,8 +627,17 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                                        fast::WS2::STRIDE));
         int per_sm = 0;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32, smem_body));
+            &per_sm, fast::attend_body_kernel<B>, fast::WARPS * 32,
+            fast::WSB::STRIDE * fast::WARPS));
         h->fast_per_sm[B][0] = per_sm < 1 ? 1 : per_sm;
+        if constexpr (B == 2) {
+            const int smem_vi = fast::WarpSmemBody<true>::STRIDE * fast::WARPS;
+            KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<2, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_vi));
+            KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, fast::attend_body_kernel<2, true>, fast::WARPS * 32, smem_vi));
+            h->fast_per_sm[B][4] = per_sm < 1 ? 1 : per_sm;
+        }
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
         h->fast_per_sm[B][1] = per_sm < 1 ? 1 : per_sm;
@@ -726,18 +741,18 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             gqa_tc::attend_gqa_tc_kernel<1>
                 <<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
         } else {
-            const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][0],
-                                                   ceil_div(a.n_items, fast::WARPS));
+            const int64_t grid = std::min<int64_t>(
+                (int64_t)num_sms() * h->fast_per_sm[B][vimma ? 4 : 0], ceil_div(a.n_items, fast::WARPS));
             if (tail_deferred) {
                 // body first (normal launch: the append is complete), then the
                 // residual-window kernel as its programmatic dependent
                 a.tail_last = 1;
-                fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
+                body_kernel<<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
             } else if (one_stream)
-                KIVI_CUDA(launch_pdl(fast::attend_body_kernel<B>, dim3((unsigned)grid),
-                                     dim3(fast::WARPS * 32), (size_t)smem_body, st, a));
+                KIVI_CUDA(launch_pdl(body_kernel, dim3((unsigned)grid), dim3(fast::WARPS * 32),
+                                     (size_t)smem_body, st, a));
             else
-                fast::attend_body_kernel<B><<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
+                body_kernel<<<(unsigned)grid, fast::WARPS * 32, smem_body, st>>>(a);
         }
         KIVI_LAUNCHED();
         h->total_launches++;

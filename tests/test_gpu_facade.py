@@ -33,21 +33,15 @@ def test_reference_unit_tests_pass_against_facade():
 
 
 def test_reference_acceptance_against_facade():
-    """Criteria 2, 3 and 8 (streaming==batch bit-exact, attention fidelity
-    incl. passthrough bit-exactness, residual window) are the hot path and
-    must pass.  Criterion 1's 10 s wall-clock bound and 2's 30 s bound time
-    3x10^5 / 2x10^4 single-group round trips to the GPU; they are reported,
-    not required (DESIGN.md "facade")."""
+    """All eight acceptance criteria pass through the facade, including the
+    wall-clock bounds: criterion 1 runs 3x10^5 quantize_group +
+    dequantize_group round trips within its 10 s (the facade dequantizes a
+    group on the device in the same round trip as its quantization) and
+    criterion 2 its 200 streaming cases within 30 s."""
     r = _run("facade_acceptance", timeout=1800)
     print(r.stdout)
     lines = {int(l.split("criterion ")[1].split(":")[0]): l for l in r.stdout.splitlines()
              if l.startswith("[")}
-    for c in (3, 4, 5, 6, 7, 8):
+    for c in range(1, 9):
         assert lines.get(c, "").startswith("[PASS]"), lines.get(c)
-    for c in (1, 2):
-        line = lines.get(c, "")
-        detail = line.split(" -- ", 1)[1] if " -- " in line else ""
-        # a FAIL here may only be the wall-clock bound ("... groups/cases in N s")
-        assert line.startswith("[PASS]") or (" in " in detail and "violated" not in detail and
-                                             "not exact" not in detail and
-                                             "mismatch" not in detail), line
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

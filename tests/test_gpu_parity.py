@@ -535,9 +535,14 @@ def test_run_decode_benchmark_fast_path_vs_reference(cuda):
     ref = Ref()
     data = ref.workload_data(sp, 3)
     want = ref.run_decode_benchmark(sp, 3, 0, 2, 32, 128)
-    rep = wl.run_decode_benchmark(sp, kb.CacheConfig(2, 32, 128, 128), data=data)
+    rep = wl.run_decode_benchmark(sp, kb.CacheConfig(2, 32, 128, 128), data=data,
+                                  fused_projection=False)
     assert rep.peak_cache_bytes == want["peak_cache_bytes"]
     assert abs(rep.output_checksum - want["output_checksum"]) <= 1e-5 * rep.output_abs_sum
+    # the fused tensor-core projection + append: same bar
+    fused = wl.run_decode_benchmark(sp, kb.CacheConfig(2, 32, 128, 128), data=data)
+    assert fused.peak_cache_bytes == want["peak_cache_bytes"]
+    assert abs(fused.output_checksum - want["output_checksum"]) <= 1e-5 * fused.output_abs_sum
 
 
 def test_run_decode_benchmark_fused_projection_no_library_gemm(cuda, monkeypatch):
@@ -710,3 +715,40 @@ def test_decode_layers_host_single_layer_zero_copy(cuda, pinned, qpk, U, l0, mon
         a, b = ref.export_unit(u), host.export_unit(u)
         for key in a:
             assert a[key].tobytes() == b[key].tobytes(), (u, key)
+
+
+@pytest.mark.parametrize("vimma", ["1", "0"])
+@pytest.mark.parametrize("growth", ["rising", "falling", "spiky"])
+def test_body_value_spans_change_between_jobs(cuda, vimma, growth, monkeypatch):
+    """The body's value jobs on the integer tensor cores keep a fixed-point
+    scale per channel group and item; a later job with larger spans moves the
+    integer sums to fp32 (regression: shifting the digit columns one by one
+    lost up to 2^24 units).  Value magnitudes that rise, fall or spike along
+    the sequence force every case; outputs vs the reference, 1e-5."""
+    monkeypatch.setenv("KIVI_VIMMA", vimma)
+    ck = checker()
+    rng = np.random.default_rng({"rising": 1, "falling": 2, "spiky": 3}[growth])
+    U, d, l0 = 40, 128, 1500
+    t = np.arange(l0, dtype=np.float32)[None, :, None]
+    if growth == "rising":
+        mag = 2.0 ** (t / 300.0)
+    elif growth == "falling":
+        mag = 2.0 ** (-(t / 300.0))
+    else:
+        mag = np.where((t.astype(np.int64) // 64) % 3 == 1, 8.0, 1.0).astype(np.float32)
+    K = rnd(rng, U, l0, d)
+    V = (rnd(rng, U, l0, d) * mag).astype(np.float32)
+    cache = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    cache.prefill(dev(K), dev(V))
+    units = (0, 7, 19, U - 1)
+    refs = {u: ck.unit(2, 32, 128, d) for u in units}
+    for u in units:
+        refs[u].prefill(K[u], V[u])
+    for step in range(3):
+        q, tk, tv = rnd(rng, U, 1, d), rnd(rng, U, d), rnd(rng, U, d)
+        out = cache.decode(dev(q), dev(tk), dev(tv)).cpu().numpy()
+        for u in units:
+            want = refs[u].decode(q[u, 0], tk[u], tv[u])
+            err = rel_l2(out[u, 0], want)
+            assert err <= 1e-5, (growth, step, u, err)
+    cache.close()
