@@ -27,12 +27,14 @@
 // Keys (per 32-token tile T, per 16-channel K step):
 //   D[token row][n = 2h + part] += A[row][k] * B[k][n]
 //   A = codes: lane (g, t) holds the byte (g & 3) of word (channel, half
-//       g >> 2), i.e. tokens 4g..4g+3 of its 4 channels 16s + 4t + {0..3};
+//       g >> 2), i.e. tokens 4g..4g+3 of its 4 channels 8s + 2t + {0, 1}
+//       and 64 + 8s + 2t + {0, 1} (K step s: channels 8s.., 64+8s..);
 //       one PRMT pairs channels (c, c+1) into the two fp16 halves and a
 //       LOP3 (after one shared shift) per token position j selects the code:
 //       row g <-> token 4g + 2m, row g+8 <-> 4g + 2m + 1 in MMA m (m = 0, 1).
 //   B = split(q'_h[c] * s_T[c] * 2^E), built cooperatively per tile (lane L
-//       computes the 16 products of channels 4L..4L+3) and stored in fragment
+//       computes the 16 products of channels 2L, 2L+1, 64+2L, 65+2L:
+//       conflict-free pair loads) and stored in fragment
 //       order in shared memory.
 //   The epilogue needs no reduction: lane (g, t) owns head t, tokens 4g+j.
 //   bias_h(T) = sum_c q'_h[c] z_T[c] is an fp32 dot product reduced through
@@ -88,9 +90,18 @@ constexpr uint32_t FULL = 0xffffffffu;
 // probs layout: token pairs (t, t+4) with t & 4 == 0 side by side per head,
 // so the value producer reads (p_h[t], p_h[t+4]) as one float2:
 //   pidx(t, h) = ((t >> 3) * 4 + (t & 3)) * 2H + 2h + ((t >> 2) & 1)
+// H = 4: the four pair blocks of a 32-word row are XOR-swizzled by the row
+// (bits 3-4 ^= (t >> 3) & 3): the key epilogue's stores (lanes g = 0..7 on
+// tokens 4g + j) then spread over 32 banks instead of 8.
 template <int H>
 __device__ __forceinline__ int pidx(int t, int h) {
-    return ((t >> 3) * 4 + (t & 3)) * (2 * H) + 2 * h + ((t >> 2) & 1);
+    const int i = ((t >> 3) * 4 + (t & 3)) * (2 * H) + 2 * h + ((t >> 2) & 1);
+    return H == 4 ? i ^ (((t >> 3) & 3) << 3) : i;
+}
+// logical pair block of physical block p (the swizzle is an involution)
+template <int H>
+__device__ __forceinline__ int pblock(int p) {
+    return H == 4 ? p ^ ((p >> 2) & 3) : p;
 }
 
 template <int H>
@@ -191,14 +202,14 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
                                         uint32_t sel, int ntl) {
     const int g = lane >> 2, t = lane & 3;
     const float4* pairs4 = reinterpret_cast<const float4*>(slot + KT * 1024);
-    // pre-pass over this lane's channels 4L..4L+3 of the KT tiles: spans,
+    // pre-pass over this lane's channels (2L, 2L+1, 64+2L, 65+2L) of the KT tiles: spans,
     // bias partials, job-wide span maximum
     float dmax = 0.f;
 #pragma unroll
     for (int T = 0; T < KT; ++T) {
         if (T < ntl) {  // tiles past a partial item's end were not loaded
-            const float4 p01 = pairs4[T * 64 + 2 * lane];
-            const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
+            const float4 p01 = pairs4[T * 64 + lane];
+            const float4 p23 = pairs4[T * 64 + 32 + lane];
             const float lo[4] = {p01.x, p01.z, p23.x, p23.z};
             dmax = fmaxf(dmax, fmaxf(fmaxf(p01.y - p01.x, p01.w - p01.z),
                                      fmaxf(p23.y - p23.x, p23.w - p23.z)));
@@ -235,8 +246,8 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     // producer: B fragments of tile T into buffer T & 1
     auto produce = [&](int T) {
         uint2* bfk = reinterpret_cast<uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
-        const float4 p01 = pairs4[T * 64 + 2 * lane];
-        const float4 p23 = pairs4[T * 64 + 2 * lane + 1];
+        const float4 p01 = pairs4[T * 64 + lane];
+        const float4 p23 = pairs4[T * 64 + 32 + lane];
         const float2 f2 = make_float2(f, f);
         const float2 d01 = __fmul2_rn(make_float2(p01.y - p01.x, p01.w - p01.z), f2);
         const float2 d23 = __fmul2_rn(make_float2(p23.y - p23.x, p23.w - p23.z), f2);
@@ -260,11 +271,14 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
         const uint8_t* ct = slot + T * 1024 + 4 * (g >> 2);
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            const int cb = (16 * s + 4 * t) * 8;
+            // K step s: channels 8s .. 8s+7 (K 2t, 2t+1 <-> 8s + 2t + {0, 1})
+            // and 64 + 8s .. 64 + 8s + 7 (K 2t+8, 2t+9), as the producer lane
+            // 4s + t built them (its pairs: channels 2L, 2L+1, 64+2L, 65+2L)
+            const int cb = (8 * s + 2 * t) * 8;
             const uint32_t w0 = *reinterpret_cast<const uint32_t*>(ct + cb);
             const uint32_t w1 = *reinterpret_cast<const uint32_t*>(ct + cb + 8);
-            const uint32_t w2 = *reinterpret_cast<const uint32_t*>(ct + cb + 16);
-            const uint32_t w3 = *reinterpret_cast<const uint32_t*>(ct + cb + 24);
+            const uint32_t w2 = *reinterpret_cast<const uint32_t*>(ct + cb + 512);
+            const uint32_t w3 = *reinterpret_cast<const uint32_t*>(ct + cb + 520);
             const CodeQuad c01 = code_quad(__byte_perm(w0, w1, sel));
             const CodeQuad c23 = code_quad(__byte_perm(w2, w3, sel));
             uint2 b = make_uint2(0u, 0u);
@@ -280,11 +294,11 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
         if (t < H) {
             // tokens tb + j, j = 0..3 share the pair block of tb (tb & 3 == 0)
             const int tb = tok0 + T * 32 + 4 * g;
-            float* dst = probs + pidx<H>(tb, t);
-            dst[0 * 2 * H] = fmaf(acc0.x + acc0.y, unscale(eb, code_pos(0)), bias);
-            dst[1 * 2 * H] = fmaf(acc0.z + acc0.w, unscale(eb, code_pos(1)), bias);
-            dst[2 * 2 * H] = fmaf(acc1.x + acc1.y, unscale(eb, code_pos(2)), bias);
-            dst[3 * 2 * H] = fmaf(acc1.z + acc1.w, unscale(eb, code_pos(3)), bias);
+            // tokens tb + j sit in pair blocks j of one row (swizzled: j ^ r)
+            probs[pidx<H>(tb + 0, t)] = fmaf(acc0.x + acc0.y, unscale(eb, code_pos(0)), bias);
+            probs[pidx<H>(tb + 1, t)] = fmaf(acc0.z + acc0.w, unscale(eb, code_pos(1)), bias);
+            probs[pidx<H>(tb + 2, t)] = fmaf(acc1.x + acc1.y, unscale(eb, code_pos(2)), bias);
+            probs[pidx<H>(tb + 3, t)] = fmaf(acc1.z + acc1.w, unscale(eb, code_pos(3)), bias);
         }
     };
     // two fragment buffers: one warp barrier per tile orders producer and
@@ -345,7 +359,7 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
     if (wlog) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int b = lane + 32 * i;
+            const int b = pblock<H>(lane + 32 * i);
             const int tb = (b >> 2) * 8 + (b & 3);
 #pragma unroll
             for (int h = 0; h < H; ++h) {
@@ -647,9 +661,11 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
                 const float2 qs2 = make_float2(a.qscale, a.qscale);
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float4 q4 = reinterpret_cast<const float4*>(qraw + h * D)[lane];
-                    qv[h][0] = __fmul2_rn(make_float2(q4.x, q4.y), qs2);
-                    qv[h][1] = __fmul2_rn(make_float2(q4.z, q4.w), qs2);
+                    // this lane's key channels: 2L, 2L+1 and 64+2L, 65+2L
+                    const float2 q01 = reinterpret_cast<const float2*>(qraw + h * D)[lane];
+                    const float2 q23 = reinterpret_cast<const float2*>(qraw + h * D + 64)[lane];
+                    qv[h][0] = __fmul2_rn(q01, qs2);
+                    qv[h][1] = __fmul2_rn(q23, qs2);
                     qmax = fmaxf(qmax, fmaxf(fmaxf(fabsf(qv[h][0].x), fabsf(qv[h][0].y)),
                                              fmaxf(fabsf(qv[h][1].x), fabsf(qv[h][1].y))));
                 }
