@@ -39,44 +39,81 @@ __device__ __forceinline__ double group_scale(float lo, float hi, int maxc) {
 
 struct CodeCtx {
     float lo;
-    float r;        // maxc / (hi - lo) in fp32
-    double lo_d;
-    double s;       // exact reference scale
+    float hi;
+    float r;        // maxc / (hi - lo) in fp32; 0 for a degenerate group, NaN
+                    // when the fp32 path cannot be used (every code exact)
+    float tie;      // 0.5 - maxc * 2^-20: fp32 decisions closer to a tie go exact
     int maxc;
-    bool degenerate;
-    bool fast_ok;
 };
 
 __device__ __forceinline__ CodeCtx make_code_ctx(float lo, float hi, int maxc) {
     CodeCtx c;
     c.lo = lo;
-    c.lo_d = (double)lo;
+    c.hi = hi;
     c.maxc = maxc;
-    c.degenerate = (hi == lo);
-    c.s = group_scale(lo, hi, maxc);
-    float span = hi - lo;
-    c.r = (float)maxc / span;
-    c.fast_ok = !c.degenerate && isfinite(c.r) && c.r > 0.0f;
+    const float r = (float)maxc / (hi - lo);
+    c.r = (hi == lo) ? 0.0f : ((isfinite(r) && r > 0.0f) ? r : __int_as_float(0x7fc00000));
+    c.tie = 0.5f - (float)maxc * 0x1p-20f;
     return c;
 }
 
+// The reference's own expression, rint((double(v) - lo) / s) clamped, with
+// the exact double scale (a DDIV: only for the rare near-tie values).
+__device__ __noinline__ uint32_t quant_code_exact(float lo, float hi, int maxc, float v) {
+    double q = rint(__ddiv_rn(__dsub_rn((double)v, (double)lo), group_scale(lo, hi, maxc)));
+    q = fmin(fmax(q, 0.0), (double)maxc);
+    return (uint32_t)q;
+}
+
+// Branch-free fp32 decision.  x = (v - lo) * r carries at most ~4 fp32
+// roundings relative to the exact quotient X <= maxc (|x - X| < 4.1 * 2^-24 *
+// maxc), so rint(x) is the reference's code unless x lies within maxc * 2^-20
+// (4x that bound) of a .5 tie; then *exact is set and the caller re-decides
+// the code by quant_code_exact.  rint by the 1.5 * 2^23 magic add
+// (round-to-nearest-even, |x| < 2^22), the code read from the sum's mantissa:
+// full-rate FADD / IADD only (floorf, rintf and F2I run on the quarter-rate
+// conversion pipe).  NaN x (r = NaN, inf inputs) always fails the test.
+__device__ __forceinline__ uint32_t quant_code_fast(const CodeCtx& c, float v, bool& exact) {
+    const float x = __fmul_rn(__fsub_rn(v, c.lo), c.r);
+    const float y = __fadd_rn(x, 12582912.0f);
+    const float rx = __fsub_rn(y, 12582912.0f);
+    exact = !(fabsf(__fsub_rn(x, rx)) < c.tie);
+    return (uint32_t)min(max(__float_as_int(y) - 0x4B400000, 0), c.maxc);
+}
+
 __device__ __forceinline__ uint32_t quant_code(const CodeCtx& c, float v) {
-    if (c.degenerate) return 0u;
-    if (c.fast_ok) {
-        float x = (v - c.lo) * c.r;
-        if (isfinite(x)) {
-            float fl = floorf(x);
-            float frac = x - fl;
-            if (fabsf(frac - 0.5f) > 1e-3f) {
-                float q = rintf(x);
-                q = fminf(fmaxf(q, 0.0f), (float)c.maxc);
-                return (uint32_t)q;
+    bool exact;
+    const uint32_t q = quant_code_fast(c, v, exact);
+    return exact ? quant_code_exact(c.lo, c.hi, c.maxc, v) : q;
+}
+
+// std::minmax_element over x[0..N) (first smallest, last largest) for finite
+// inputs: FMNMX chains, then the only case where equal-comparing values have
+// different bits, +0 / -0, re-resolved in order.  (Non-finite groups are out
+// of contract: the reference's own codes are undefined for NaN.)
+template <int N>
+__device__ __forceinline__ float2 minmax_first_last(const float (&x)[N]) {
+    float lo = x[0], hi = x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+        lo = fminf(lo, x[i]);
+        hi = fmaxf(hi, x[i]);
+    }
+    if (lo == 0.0f || hi == 0.0f) {
+        float zf = 0.0f, zl = 0.0f;
+        bool seen = false;
+#pragma unroll
+        for (int i = N - 1; i >= 0; --i) {
+            if (x[i] == 0.0f) {
+                zf = x[i];            // ends as the first zero
+                if (!seen) zl = x[i];  // the last zero
+                seen = true;
             }
         }
+        if (lo == 0.0f) lo = zf;
+        if (hi == 0.0f) hi = zl;
     }
-    double q = rint(__ddiv_rn(__dsub_rn((double)v, c.lo_d), c.s));
-    q = fmin(fmax(q, 0.0), (double)c.maxc);
-    return (uint32_t)q;
+    return make_float2(lo, hi);
 }
 
 // Reference dequantisation: float(double(code) * s + z), no contraction

@@ -39,7 +39,7 @@ __device__ __forceinline__ float2 quantize_group_dev(const float* p, int64_t str
     float lo = p[0], hi = p[0];
     for (int i = 1; i < G; ++i) minmax_step(p[(int64_t)i * stride], lo, hi);
     CodeCtx cc = make_code_ctx(lo, hi, maxc);
-    if (!cc.degenerate) {
+    if (hi != lo) {
         // Accumulate whole 32-bit words, flush each once.
         uint64_t bit = bit0;
         uint32_t word = 0;
@@ -97,25 +97,35 @@ __global__ void prefill_values_kernel(CacheDev c, const float* __restrict__ valu
 }
 
 // Residual rows: keys [kg, l) -> ring rows [0, l-kg); values [vg, l) -> rows t % R.
+// vec = 4 (d % 4 == 0, 16-byte aligned rows): one float4 per thread;
+// otherwise (vec = 1) one float per thread.
 __global__ void prefill_residual_kernel(CacheDev c, const float* __restrict__ keys,
                                         const float* __restrict__ values, int64_t l, int64_t kg,
-                                        int64_t vg) {
+                                        int64_t vg, int vec) {
     const int64_t kr = l - kg, vr = l - vg;
-    const int64_t per_unit = (kr + vr) * c.d;
+    const int64_t rowv = c.d / vec;  // vectors per row
+    const int64_t per_unit = (kr + vr) * rowv;
     const int64_t total = per_unit * c.n_units;
     for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
          gid += (int64_t)gridDim.x * blockDim.x) {
         const int64_t u = gid / per_unit;
-        int64_t e = gid % per_unit;
-        const int64_t ch = e % c.d;
-        int64_t row = e / c.d;
+        const int64_t e = gid - u * per_unit;
+        const int64_t row = e / rowv;
+        const int64_t ch = (e - row * rowv) * vec;
+        const float* src;
+        float* dst;
         if (row < kr) {
-            const int64_t t = kg + row;
-            c.kring[u * c.ring_ustride + row * c.d + ch] = keys[(u * l + t) * c.d + ch];
+            src = keys + (u * l + kg + row) * c.d + ch;
+            dst = c.kring + u * c.ring_ustride + row * c.d + ch;
         } else {
             const int64_t t = vg + (row - kr);
-            c.vring[u * c.ring_ustride + (t % c.R) * c.d + ch] = values[(u * l + t) * c.d + ch];
+            src = values + (u * l + t) * c.d + ch;
+            dst = c.vring + u * c.ring_ustride + (t % c.R) * c.d + ch;
         }
+        if (vec == 4)
+            *reinterpret_cast<float4*>(dst) = __ldcs(reinterpret_cast<const float4*>(src));
+        else
+            *dst = *src;
     }
 }
 
@@ -191,18 +201,41 @@ template <int B>
 __device__ __forceinline__ void value_row_fast(const float4 v, int lane, uint32_t* __restrict__ vw,
                                                float2* __restrict__ vp) {
     const float x[4] = {v.x, v.y, v.z, v.w};
-    float lo = x[0], hi = x[0];
-    int ilo = 4 * lane, ihi = 4 * lane;
+    float lo = fminf(fminf(x[0], x[1]), fminf(x[2], x[3]));
+    float hi = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
 #pragma unroll
-    for (int i = 1; i < 4; ++i) {
-        if (x[i] < lo) { lo = x[i]; ilo = 4 * lane + i; }
-        if (!(x[i] < hi)) { hi = x[i]; ihi = 4 * lane + i; }
+    for (int o = 1; o < 8; o <<= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    minmax_pair_reduce8(lo, ilo, hi, ihi);
-    const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
-    uint32_t bits = 0;
+    if (__any_sync(0xffffffffu, lo == 0.0f || hi == 0.0f)) {
+        // a zero extreme: +0 / -0 compare equal, so resolve first smallest /
+        // last largest by channel index (rare; warp-uniform branch)
+        lo = x[0];
+        hi = x[0];
+        int ilo = 4 * lane, ihi = 4 * lane;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) bits |= quant_code(cc, x[i]) << (B * i);
+        for (int i = 1; i < 4; ++i) {
+            if (x[i] < lo) { lo = x[i]; ilo = 4 * lane + i; }
+            if (!(x[i] < hi)) { hi = x[i]; ihi = 4 * lane + i; }
+        }
+        minmax_pair_reduce8(lo, ilo, hi, ihi);
+    }
+    const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+    uint32_t bits = 0, redo = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        bool ex;
+        bits |= quant_code_fast(cc, x[i], ex) << (B * i);
+        redo |= (uint32_t)ex << i;
+    }
+    if (redo) {  // rare: near-tie values decided exactly
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (redo & (1u << i))
+                bits = (bits & ~(((1u << B) - 1u) << (B * i))) |
+                       (quant_code_exact(lo, hi, (1 << B) - 1, x[i]) << (B * i));
+    }
     // lane's 4 codes -> position (4*lane*B) of the token's 128*B-bit row
     uint32_t word = bits << ((4 * lane * B) & 31);
     constexpr int LPW = 32 / (4 * B);  // lanes sharing one 32-bit word
@@ -212,24 +245,37 @@ __device__ __forceinline__ void value_row_fast(const float4 v, int lane, uint32_
     if ((lane & 7) == 0) vp[lane >> 3] = make_float2(lo, hi);
 }
 
-// One per-channel key group (32 tokens of one channel, in token order) ->
-// its B code words (token i at bits B*(i % (32/B)) of word i / (32/B)) and
+// One group of 32 values in stream order (a key group: 32 tokens of one
+// channel; a value group: 32 channels of one token) -> its B code words (token i at bits B*(i % (32/B)) of word i / (32/B)) and
 // (lo, hi); sequential over the tokens, so first-min / last-max are exact.
 template <int B>
 __device__ __forceinline__ float2 key_group_fast(const float (&x)[32], uint32_t (&w)[B]) {
-    float lo = x[0], hi = x[0];
-#pragma unroll
-    for (int i = 1; i < 32; ++i) minmax_step(x[i], lo, hi);
-    const CodeCtx cc = make_code_ctx(lo, hi, (1 << B) - 1);
+    const float2 lh = minmax_first_last(x);
+    const CodeCtx cc = make_code_ctx(lh.x, lh.y, (1 << B) - 1);
     constexpr int CPW = 32 / B;  // codes per word
+    uint32_t redo = 0;           // values whose code must be decided exactly
 #pragma unroll
     for (int k = 0; k < B; ++k) {
         uint32_t word = 0;
 #pragma unroll
-        for (int i = 0; i < CPW; ++i) word |= quant_code(cc, x[k * CPW + i]) << (B * i);
+        for (int i = 0; i < CPW; ++i) {
+            bool ex;
+            word |= quant_code_fast(cc, x[k * CPW + i], ex) << (B * i);
+            redo |= (uint32_t)ex << (k * CPW + i);
+        }
         w[k] = word;
     }
-    return make_float2(lo, hi);
+    if (redo) {  // rare (near-tie values, non-finite groups)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (redo & (1u << j)) {
+                const int k = j / CPW, sh = B * (j % CPW);
+                const uint32_t q = quant_code_exact(cc.lo, cc.hi, cc.maxc, x[j]);
+                w[k] = (w[k] & ~(((1u << B) - 1u) << sh)) | (q << sh);
+            }
+        }
+    }
+    return lh;
 }
 
 template <int B>
@@ -309,18 +355,27 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
     append_unit_fast<B, false>(c, tk, tv, l, u, lane);
 }
 
-// The append of a flush step ((l + 1) % R == 0): blocks [0, n_app) append one
-// unit per warp (no flush); the remaining blocks flush the key ring, one
-// thread per (unit, 32-token tile, channel) group: lanes are 32 consecutive
-// channels, so every token row is one coalesced 128-byte load per warp and the
-// group's code words one contiguous store.  The ring's last row (token l) is
-// read from t_k, which the append warps write concurrently; with t_k == NULL
-// (n_app = 0: the projection kernel already wrote the row) from the ring.
+// Append plus early key-tile quantisation: blocks [0, n_app) append one unit
+// per warp (no flush); the remaining blocks quantize ring tiles
+// [tl0, tl0 + ntl) of the current window (kg = l - l % R), one thread per
+// (unit, 32-token tile, channel) group: lanes are 32 consecutive channels, so
+// every token row is one coalesced 128-byte load per warp and the group's
+// code words one contiguous store.
+//
+// A key tile is quantized as soon as its 32 rows are in the ring, not all
+// R / 32 at the flush: the attend kernels and every export read codes of
+// tiles below kg only, the rows stay fp32 in the ring until the flush
+// (kv_cache.cpp:80-90), and a tile's codes depend on its own 32 rows only —
+// so the flush step's work is one tile, not R / 32 (kivi_cache::kq_done).
+// Row l % R (token l) is read from t_k, which the append warps write
+// concurrently; with t_k == NULL (n_app = 0: the projection kernel already
+// wrote the row) from the ring.
 template <int B>
 __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
                                                                 const float* __restrict__ tk,
                                                                 const float* __restrict__ tv,
-                                                                int64_t l, int n_app) {
+                                                                int64_t l, int n_app, int tl0,
+                                                                int ntl) {
     pdl_trigger();
     constexpr int D = 128, G = 32;
     const int lane = threadIdx.x & 31;
@@ -329,15 +384,14 @@ __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
         if (u < c.n_units) append_unit_fast<B, false>(c, tk, tv, l, u, lane);
         return;
     }
-    const int tiles = c.R / G;
     const int64_t fw = (int64_t)(blockIdx.x - n_app) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t u = fw / (tiles * (D / 32));
+    const int64_t u = fw / (ntl * (D / 32));
     if (u >= c.n_units) return;
-    const int rem = (int)(fw % (tiles * (D / 32)));
-    const int tl = rem / (D / 32);
+    const int rem = (int)(fw % (ntl * (D / 32)));
+    const int tl = tl0 + rem / (D / 32);
     const int ch = (rem % (D / 32)) * 32 + lane;
     const float* kring = c.kring + u * c.ring_ustride;
-    const int last = c.R - 1;  // ring row of token l (written by this launch)
+    const int last = (int)(l % c.R);  // ring row of token l (written by this launch)
     float x[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -346,7 +400,7 @@ __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
     }
     uint32_t w[B];
     const float2 lh = key_group_fast<B>(x, w);
-    const int64_t g = ((l + 1 - c.R) / G + tl) * D + ch;
+    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
     store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
     c.kpairs[u * c.kp_ustride + g] = lh;
 }
@@ -377,23 +431,37 @@ __global__ void __launch_bounds__(256) prefill_keys_fast_kernel(CacheDev c,
     }
 }
 
-// Values: one warp per token row (512 B, one float4 per lane), the row's four
-// 32-channel groups reduced across 8 lanes each (value_row_fast).
+// Values: one thread per (unit, token, 32-channel group): the group's 128
+// contiguous bytes as 8 float4 loads (a warp's first load touches 32 lines,
+// the next seven hit the sectors L1 already holds), min / max and codes in
+// registers exactly as for a key group — no cross-lane reductions, ~1/3 of
+// the instructions of a warp-per-row split.  Group g = t * 4 + cg of a unit
+// has its codes at word g * B and its pair at g, as a key group does.
 template <int B>
 __global__ void __launch_bounds__(256) prefill_values_fast_kernel(CacheDev c,
                                                                   const float* __restrict__ values,
                                                                   int64_t l, int64_t vg) {
     constexpr int D = 128, G = 32;
-    const int lane = threadIdx.x & 31;
-    const int64_t rows = vg * c.n_units;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
-         r += nw) {
-        const int64_t u = r / vg, t = r % vg;
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(values + (u * l + t) * D) + lane);
-        value_row_fast<B>(v, lane,
-                          reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + t * (D * B / 32),
-                          c.vpairs + u * c.vp_ustride + t * (D / G));
+    const int64_t per_unit = vg * (D / G);
+    const int64_t total = per_unit * c.n_units;
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = gid / per_unit;
+        const int64_t g = gid - u * per_unit;  // t * 4 + cg
+        const float4* src = reinterpret_cast<const float4*>(values + u * l * D + g * G);
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 v = __ldcs(src + i);
+            x[4 * i] = v.x;
+            x[4 * i + 1] = v.y;
+            x[4 * i + 2] = v.z;
+            x[4 * i + 3] = v.w;
+        }
+        uint32_t w[B];
+        const float2 lh = key_group_fast<B>(x, w);
+        store_key_words<B>(reinterpret_cast<uint32_t*>(c.vcodes + u * c.v_ustride) + g * B, w);
+        c.vpairs[u * c.vp_ustride + g] = lh;
     }
 }
 
@@ -539,7 +607,7 @@ __global__ void quantize_codes_kernel(const float* __restrict__ m, int64_t rows,
         const CodeCtx cc = make_code_ctx(lo, hi, maxc);
         for (int i = 0; i < G; ++i) codes[g * G + i] = (uint8_t)quant_code(cc, src[(int64_t)i * stride]);
         zp[g] = (double)lo;
-        sc[g] = cc.s;
+        sc[g] = group_scale(lo, hi, maxc);
     }
 }
 

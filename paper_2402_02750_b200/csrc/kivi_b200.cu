@@ -108,6 +108,10 @@ struct kivi_cache {
     int64_t cap = 0;  // tokens per unit (multiple of R)
     int64_t l = 0;
     int64_t kres_cap = 0, vres_cap = 0;  // reference residual_capacity
+    // Complete 32-row key tiles of the current ring window whose codes are
+    // already in kcodes (quantized early by the fast append, see
+    // append_flush_fast_kernel); reset at every flush, prefill and import.
+    int64_t kq_done = 0;
     int attend_path = 0;
     CacheDev dev{};
 
@@ -300,6 +304,13 @@ kivi_status ensure(T** p, int64_t* cap, int64_t need) {
 kivi_status ensure_capacity(kivi_cache* h, int64_t tokens, cudaStream_t st) {
     if (tokens <= h->cap) return KIVI_OK;
     return kivi_cache_reserve(h, std::max<int64_t>(tokens, 2 * h->cap), st);
+}
+
+// The fast kernels move caller rows as 16-byte vectors and TMA bulk copies:
+// they need 16-byte aligned row pointers (d = 128 keeps every row aligned).
+bool al16(const void* a, const void* b = nullptr, const void* c = nullptr,
+          const void* d = nullptr, const void* e = nullptr) {
+    return ((((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)d | (uintptr_t)e) & 15) == 0);
 }
 
 bool fast_supported(const kivi_cache* h, int qpk) {
@@ -1108,6 +1119,7 @@ kivi_status kivi_cache_clone(const kivi_cache* src, void* stream, kivi_cache** o
                               cudaMemcpyDeviceToDevice, st));
     KIVI_CUDA(cudaStreamSynchronize(st));
     h->l = src->l;
+    h->kq_done = src->kq_done;
     h->kres_cap = src->kres_cap;
     h->vres_cap = src->vres_cap;
     h->attend_path = src->attend_path;
@@ -1159,7 +1171,9 @@ kivi_status kivi_prefill(kivi_cache* h, const float* keys, const float* values, 
     const int64_t kg = l - l % R;
     const int64_t vg = l - std::min(l, R);
     const int64_t G = h->cfg.group_size, d = h->cfg.head_dim;
-    const bool fast = d == 128 && G == 32 && (c.bits == 2 || c.bits == 4);
+    // the fast kernels read 16-byte vectors of the caller's rows
+    const bool rows16 = (((uintptr_t)keys | (uintptr_t)values) & 15) == 0;
+    const bool fast = d == 128 && G == 32 && (c.bits == 2 || c.bits == 4) && rows16;
     if (kg > 0) {
         if (fast && c.bits == 2)
             prefill_keys_fast_kernel<2><<<grid_for(U * (kg / G) * d), 256, 0, st>>>(c, keys, l, kg);
@@ -1172,19 +1186,21 @@ kivi_status kivi_prefill(kivi_cache* h, const float* keys, const float* values, 
     }
     if (vg > 0) {
         if (fast && c.bits == 2)
-            prefill_values_fast_kernel<2><<<grid_for(U * vg * 32), 256, 0, st>>>(c, values, l, vg);
+            prefill_values_fast_kernel<2><<<grid_for(U * vg * 4), 256, 0, st>>>(c, values, l, vg);
         else if (fast)
-            prefill_values_fast_kernel<4><<<grid_for(U * vg * 32), 256, 0, st>>>(c, values, l, vg);
+            prefill_values_fast_kernel<4><<<grid_for(U * vg * 4), 256, 0, st>>>(c, values, l, vg);
         else
             prefill_values_kernel<<<grid_for(U * vg * (d / G)), 256, 0, st>>>(c, values, l, vg);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
-    prefill_residual_kernel<<<grid_for(U * (2 * l - kg - vg) * d), 256, 0, st>>>(c, keys, values,
-                                                                                 l, kg, vg);
+    const int vec = (d % 4 == 0 && rows16) ? 4 : 1;
+    prefill_residual_kernel<<<grid_for(U * (2 * l - kg - vg) * (d / vec)), 256, 0, st>>>(
+        c, keys, values, l, kg, vg, vec);
     KIVI_LAUNCHED();
     h->total_launches++;
     h->l = l;
+    h->kq_done = 0;
     h->kres_cap = l % R;  // kv_cache.cpp:40
     h->vres_cap = std::min(l, R);
     return KIVI_OK;
@@ -1199,23 +1215,38 @@ static void append_bookkeeping(kivi_cache* h) {
     const int64_t vrows = std::min(h->l, R) == R ? R : std::min(h->l, R) + 1;
     h->vres_cap = std::max(h->vres_cap, vrows);
     h->l += 1;
+    if (h->l % R == 0) h->kq_done = 0;  // flushed: a new ring window
+}
+
+// Key tiles the fast append of token h->l must quantize: the complete tiles
+// of the ring after the push not yet quantized, [kq_done, rows / 32) (one
+// tile every 32 steps; after a prefill or import, every complete tile).
+static void key_tiles_due(kivi_cache* h, int* tl0, int* ntl) {
+    const int64_t rows = h->l % h->cfg.residual_length + 1;
+    const int64_t done = rows / 32;
+    *tl0 = (int)h->kq_done;
+    *ntl = (int)std::max<int64_t>(done - h->kq_done, 0);
+    h->kq_done = std::max(h->kq_done, done);
 }
 
 static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t_v,
                                  cudaStream_t st) {
     const kivi_config& cf = h->cfg;
-    if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4)) {
+    if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4) &&
+        al16(t_k, t_v)) {
         const unsigned grid = (unsigned)ceil_div(h->n_units, 8);
-        if ((h->l + 1) % cf.residual_length == 0) {
-            // key flush step: extra blocks quantize the ring, one thread per group
-            const int64_t groups = h->n_units * (cf.residual_length / 32) * 128;
+        int tl0, ntl;
+        key_tiles_due(h, &tl0, &ntl);
+        if (ntl > 0) {
+            // complete key tiles: extra blocks quantize them, one thread per group
+            const int64_t groups = h->n_units * ntl * 128;
             const unsigned fgrid = (unsigned)ceil_div(groups, 256);
             if (cf.bits == 2)
                 append_flush_fast_kernel<2><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
-                                                                         (int)grid);
+                                                                         (int)grid, tl0, ntl);
             else
                 append_flush_fast_kernel<4><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
-                                                                         (int)grid);
+                                                                         (int)grid, tl0, ntl);
         } else if (cf.bits == 2) {
             append_fast_kernel<2><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
         } else {
@@ -1250,9 +1281,10 @@ kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float
     if (h->l < 1) return fail(KIVI_ERR_USAGE, "attend: empty cache");
     DeviceGuard g(h->device);
     cudaStream_t st = S(stream);
-    const bool fast_ok = fast_supported(h, q_per_kv);
+    const bool fast_ok = fast_supported(h, q_per_kv) && al16(t_q, out, weights);
     if (h->attend_path == 2 && !fast_ok)
-        return fail(KIVI_ERR_CONFIG, "fast attend path does not support this shape");
+        return fail(KIVI_ERR_CONFIG,
+                    "fast attend path does not support this shape (or rows not 16-byte aligned)");
     if (fast_ok && h->attend_path != 1) {
         const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
         const float qscale = scale * fast::LOG2E;
@@ -1271,7 +1303,8 @@ kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const
     if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
     if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL query/output");
     if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
-    if (small_fused_ok(h, q_per_kv) && fast_supported(h, q_per_kv)) {
+    const bool aligned = al16(t_q, t_k, t_v, out, weights);
+    if (small_fused_ok(h, q_per_kv) && fast_supported(h, q_per_kv) && aligned) {
         DeviceGuard g(h->device);
         cudaStream_t st = S(stream);
         kivi_status rc = ensure_capacity(h, h->l + 1, st);
@@ -1284,7 +1317,7 @@ kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const
             return launch_small_fused<2>(h, t_q, t_k, t_v, out, weights, qscale, l_app, st);
         return launch_small_fused<4>(h, t_q, t_k, t_v, out, weights, qscale, l_app, st);
     }
-    if (fused_append_ok(h, q_per_kv) && fast_supported(h, q_per_kv)) {
+    if (fused_append_ok(h, q_per_kv) && fast_supported(h, q_per_kv) && aligned) {
         // The append runs inside the residual-window kernel, on each unit right
         // before its residual items; the body items never read what it writes
         // (launch_fast stops the body at floor32(vg - 1)).
@@ -1808,7 +1841,19 @@ kivi_status launch_proj(kivi_proj* p, const float* x, int64_t n, proj::ProjArgs 
     a.split_mode = tune().proj_split;
     const size_t smem = 1024 + (size_t)a.stages * stage + (3 * a.stages + 2) * 8;
     auto kern = bits == 4 ? proj::proj_kernel<4> : proj::proj_kernel<2>;
-    KIVI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // The attribute is per function and device, shared by every host thread
+    // driving this device: always set the same value (the device's opt-in
+    // maximum), so a thread launching a small tile never lowers the limit
+    // under another thread's larger launch (a "too many resources" race).
+    {
+        int optin = 0;
+        KIVI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
+        cudaFuncAttributes fa{};
+        KIVI_CUDA(cudaFuncGetAttributes(&fa, kern));
+        const int lim = optin - (int)fa.sharedSizeBytes;
+        if ((int)smem > lim) return fail(KIVI_ERR_CONFIG, "projection: %zu B of shared memory > %d", smem, lim);
+        KIVI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    }
     const int n_tiles = (int)ceil_div(n, N);
     for (int t = 0; t < n_tiles; ++t) {  // one launch per N tile (n_valid / n_tile0 differ)
         proj::ProjArgs at = a;
@@ -1865,14 +1910,18 @@ kivi_status kivi_proj_append(kivi_proj* p, kivi_cache* h, const float* x, int64_
     rc = launch_proj(p, x, n, a, cf.bits, st);
     if (rc) return rc;
     h->total_launches += ceil_div(n, 256);
-    if ((h->l + 1) % cf.residual_length == 0) {
-        // key flush of this step: the projection wrote token l into the ring
-        const int64_t groups = h->n_units * (cf.residual_length / 32) * 128;
+    int tl0, ntl;
+    key_tiles_due(h, &tl0, &ntl);
+    if (ntl > 0) {
+        // complete key tiles of this step: the projection wrote token l into the ring
+        const int64_t groups = h->n_units * ntl * 128;
         const unsigned fgrid = (unsigned)ceil_div(groups, 256);
         if (cf.bits == 2)
-            append_flush_fast_kernel<2><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0);
+            append_flush_fast_kernel<2><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0,
+                                                              tl0, ntl);
         else
-            append_flush_fast_kernel<4><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0);
+            append_flush_fast_kernel<4><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0,
+                                                              tl0, ntl);
         KIVI_LAUNCHED();
         h->total_launches++;
     }
@@ -1966,6 +2015,7 @@ kivi_status kivi_import_unit(kivi_cache* h, int64_t unit, int64_t total_tokens,
     kivi_status rc = ensure_capacity(h, total_tokens, st);
     if (rc) return rc;
     h->l = total_tokens;
+    h->kq_done = 0;
     h->kres_cap = key_residual_capacity;
     h->vres_cap = value_residual_capacity;
     CacheDev& c = h->dev;

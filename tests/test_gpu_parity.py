@@ -160,6 +160,86 @@ def test_prefill_then_stream_state_bit_exact(cuda, cfg):
             refs[u].append(K[u, t], V[u, t])
 
 
+@pytest.mark.parametrize("bits", [2, 4])
+def test_fast_quantizer_signed_zero_and_tie_groups(cuda, bits):
+    """The d = 128, G = 32 kernels (prefill, warp-per-unit append with its
+    value pop, parallel key flush) decide codes in fp32 via the magic-number
+    rint and take min / max with FMNMX: groups whose extreme is +0 / -0 in
+    both orders, exact rounding ties (x = k + 1/2: the exact double path) and
+    all-zero groups of mixed sign must still give the reference's state."""
+    ck = checker()
+    rng = np.random.default_rng(77 + bits)
+    U, d, R, G = 4, 128, 128, 32
+    n = 3 * R + 40
+    pools = [np.array([-0.0, 0.0, 0.25, 0.75, 1.5], np.float32),   # min is a signed zero
+             np.array([-1.5, -0.25, -0.75, -0.0, 0.0], np.float32),  # max is a signed zero
+             None,                                                  # random
+             np.array([-0.0, 0.0], np.float32)]                      # all-zero groups
+    K = np.empty((U, n, d), np.float32)
+    V = np.empty((U, n, d), np.float32)
+    for u, pool in enumerate(pools):
+        if pool is None:
+            K[u], V[u] = rnd(rng, n, d), rnd(rng, n, d)
+        else:
+            K[u], V[u] = rng.choice(pool, (n, d)), rng.choice(pool, (n, d))
+    k0 = R + 45
+    cache = kb.KVCache(kb.CacheConfig(bits, G, R, d), U)
+    cache.prefill(dev(K[:, :k0]), dev(V[:, :k0]))
+    refs = [ck.unit(bits, G, R, d) for _ in range(U)]
+    for u in range(U):
+        refs[u].prefill(K[u, :k0], V[u, :k0])
+    for t in range(k0, n + 1):
+        if t in (k0, 2 * R, 2 * R + 1, 3 * R, n):
+            torch.cuda.synchronize()
+            for u in range(U):
+                assert_state_equal(cache.export_unit(u), refs[u].export(), f"t={t} u={u}")
+        if t == n:
+            break
+        cache.append(dev(K[:, t]), dev(V[:, t]))
+        for u in range(U):
+            refs[u].append(K[u, t], V[u, t])
+    cache.close()
+
+
+def test_prefill_unaligned_rows(cuda):
+    """Prefill rows that are not 16-byte aligned (a view one float into a
+    buffer) take the scalar kernels; the state is the same bit for bit."""
+    ck = checker()
+    rng = np.random.default_rng(31)
+    U, l, d = 2, 300, 128
+    K, V = rnd(rng, U, l, d), rnd(rng, U, l, d)
+    kbuf = torch.empty(U * l * d + 1, device="cuda")
+    vbuf = torch.empty(U * l * d + 1, device="cuda")
+    kv = kbuf[1:].view(U, l, d)
+    vv = vbuf[1:].view(U, l, d)
+    kv.copy_(dev(K))
+    vv.copy_(dev(V))
+    cache = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    cache.prefill(kv, vv)
+    refs = []
+    for u in range(U):
+        r = ck.unit(2, 32, 128, d)
+        r.prefill(K[u], V[u])
+        assert_state_equal(cache.export_unit(u), r.export(), f"u={u}")
+        refs.append(r)
+    # decode with unaligned q / k / v rows: routed to the generic kernels
+    for step in range(3):
+        q, tk, tv = rnd(rng, U, d), rnd(rng, U, d), rnd(rng, U, d)
+        bufs = [torch.empty(U * d + 1, device="cuda") for _ in range(3)]
+        qv, tkv, tvv = (b[1:].view(U, d) for b in bufs)
+        qv.copy_(dev(q))
+        tkv.copy_(dev(tk))
+        tvv.copy_(dev(tv))
+        out = cache.decode(qv.view(U, 1, d), tkv, tvv).cpu().numpy()
+        for u in range(U):
+            want = refs[u].decode(q[u], tk[u], tv[u])
+            assert rel_l2(out[u, 0], want) <= 1e-6, f"step {step} unit {u}"
+    torch.cuda.synchronize()
+    for u in range(U):
+        assert_state_equal(cache.export_unit(u), refs[u].export(), f"after decode u={u}")
+    cache.close()
+
+
 def test_streaming_equals_batch(cuda):
     # reference test_kv_cache.cpp:133-157 on the device path
     rng = np.random.default_rng(25)
