@@ -452,6 +452,21 @@ class LayerStack:
                                              int(bool(scale_logits)),
                                              _stream_ptr(stream, self.device)))
 
+    def bind_host_step(self, q, t_k, t_v, out, q_per_kv: int = 1, scale_logits: bool = True,
+                       stream=None):
+        """decode_host over fixed (pinned) host buffers, arguments resolved once:
+        returns a no-argument callable for a serving loop that refills the same
+        buffers every step (a latency-bound step then pays only the C call)."""
+        f = lib().kivi_decode_layers_host
+        args = (self._arr, len(self.caches), _hptr(q), _hptr(t_k), _hptr(t_v), int(q_per_kv),
+                _hptr(out), int(bool(scale_logits)), _stream_ptr(stream, self.device))
+
+        def step():
+            st = f(*args)
+            if st:
+                _check(st)
+        return step
+
 
 class Projection:
     """One layer's q/k/v projection (reference workload.cpp:230-232, x @ W) on

@@ -345,13 +345,32 @@ __device__ __forceinline__ void append_unit_fast(const CacheDev& c, const float*
     }
 }
 
+// Optional query staging (qs.src != NULL): the warp of unit u also copies
+// that unit's qs.rows query rows from qs.src (host memory mapped into the
+// device: the single-layer host path) to qs.dst, so a latency-bound step
+// needs no separate H2D copy (each costs ~15 us of DMA setup for 16 KB).
+struct QStage {
+    const float* src;
+    float* dst;
+    int rows;  // query rows (q_per_kv) per unit
+};
+
+__device__ __forceinline__ void stage_q_rows(const QStage& qs, int64_t u, int lane) {
+    if (!qs.src) return;
+    const float4* s4 = reinterpret_cast<const float4*>(qs.src + u * qs.rows * 128);
+    float4* d4 = reinterpret_cast<float4*>(qs.dst + u * qs.rows * 128);
+    for (int i = lane; i < qs.rows * 32; i += 32) d4[i] = s4[i];
+}
+
 template <int B>
 __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const float* __restrict__ tk,
-                                                          const float* __restrict__ tv, int64_t l) {
+                                                          const float* __restrict__ tv, int64_t l,
+                                                          QStage qs) {
     pdl_trigger();  // the attend launch may be scheduled behind this one
     const int lane = threadIdx.x & 31;
     const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (u >= c.n_units) return;
+    stage_q_rows(qs, u, lane);
     append_unit_fast<B, false>(c, tk, tv, l, u, lane);
 }
 
@@ -375,13 +394,16 @@ __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
                                                                 const float* __restrict__ tk,
                                                                 const float* __restrict__ tv,
                                                                 int64_t l, int n_app, int tl0,
-                                                                int ntl) {
+                                                                int ntl, QStage qs) {
     pdl_trigger();
     constexpr int D = 128, G = 32;
     const int lane = threadIdx.x & 31;
     if ((int)blockIdx.x < n_app) {
         const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-        if (u < c.n_units) append_unit_fast<B, false>(c, tk, tv, l, u, lane);
+        if (u < c.n_units) {
+            stage_q_rows(qs, u, lane);
+            append_unit_fast<B, false>(c, tk, tv, l, u, lane);
+        }
         return;
     }
     const int64_t fw = (int64_t)(blockIdx.x - n_app) * (blockDim.x >> 5) + (threadIdx.x >> 5);

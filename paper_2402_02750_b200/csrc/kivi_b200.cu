@@ -1229,11 +1229,18 @@ static void key_tiles_due(kivi_cache* h, int* tl0, int* ntl) {
     h->kq_done = std::max(h->kq_done, done);
 }
 
-static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t_v,
-                                 cudaStream_t st) {
+// qs: optional query staging by the fast append (QStage); callers check
+// append_stages_q() first.
+static bool append_stages_q(const kivi_cache* h, const float* t_k, const float* t_v) {
     const kivi_config& cf = h->cfg;
-    if (cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4) &&
-        al16(t_k, t_v)) {
+    return cf.head_dim == 128 && cf.group_size == 32 && (cf.bits == 2 || cf.bits == 4) &&
+           al16(t_k, t_v);
+}
+
+static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t_v,
+                                 cudaStream_t st, QStage qs = QStage{nullptr, nullptr, 0}) {
+    const kivi_config& cf = h->cfg;
+    if (append_stages_q(h, t_k, t_v)) {
         const unsigned grid = (unsigned)ceil_div(h->n_units, 8);
         int tl0, ntl;
         key_tiles_due(h, &tl0, &ntl);
@@ -1243,14 +1250,14 @@ static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t
             const unsigned fgrid = (unsigned)ceil_div(groups, 256);
             if (cf.bits == 2)
                 append_flush_fast_kernel<2><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
-                                                                         (int)grid, tl0, ntl);
+                                                                         (int)grid, tl0, ntl, qs);
             else
                 append_flush_fast_kernel<4><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
-                                                                         (int)grid, tl0, ntl);
+                                                                         (int)grid, tl0, ntl, qs);
         } else if (cf.bits == 2) {
-            append_fast_kernel<2><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
+            append_fast_kernel<2><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l, qs);
         } else {
-            append_fast_kernel<4><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l);
+            append_fast_kernel<4><<<grid, 256, 0, st>>>(h->dev, t_k, t_v, h->l, qs);
         }
     } else {
         append_kernel<<<(unsigned)h->n_units, 128, 0, st>>>(h->dev, t_k, t_v, h->l);
@@ -1296,14 +1303,45 @@ kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float
     return launch_generic(h, t_q, q_per_kv, out, weights, scale_logits, st);
 }
 
+static kivi_status decode_impl(kivi_cache* h, const float* t_q, const float* t_k,
+                               const float* t_v, int32_t q_per_kv, float* out, float* weights,
+                               int32_t scale_logits, void* stream, const float* q_src);
+
 kivi_status kivi_decode(kivi_cache* h, const float* t_q, const float* t_k, const float* t_v,
                         int32_t q_per_kv, float* out, float* weights, int32_t scale_logits,
                         void* stream) {
+    return decode_impl(h, t_q, t_k, t_v, q_per_kv, out, weights, scale_logits, stream, nullptr);
+}
+
+// q_src != NULL: the query rows are in device-mapped host memory at q_src and
+// t_q is device scratch; the fast append copies them across (QStage), other
+// routes enqueue a copy first.
+static kivi_status decode_impl(kivi_cache* h, const float* t_q, const float* t_k,
+                               const float* t_v, int32_t q_per_kv, float* out, float* weights,
+                               int32_t scale_logits, void* stream, const float* q_src) {
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
     if (q_per_kv < 1) return fail(KIVI_ERR_SHAPE, "q_per_kv must be >= 1");
     if (!t_q || !out) return fail(KIVI_ERR_SHAPE, "decode_attention: NULL query/output");
     if (!t_k || !t_v) return fail(KIVI_ERR_SHAPE, "append_token: NULL key/value rows");
     const bool aligned = al16(t_q, t_k, t_v, out, weights);
+    if (q_src && !(append_stages_q(h, t_k, t_v) && al16(q_src) && !small_fused_ok(h, q_per_kv) &&
+                   !fused_append_ok(h, q_per_kv))) {
+        DeviceGuard g(h->device);
+        KIVI_CUDA(cudaMemcpyAsync(const_cast<float*>(t_q), q_src,
+                                  sizeof(float) * h->n_units * q_per_kv * h->cfg.head_dim,
+                                  cudaMemcpyDefault, S(stream)));
+        q_src = nullptr;
+    }
+    if (q_src) {  // fast append stages q, then the attend
+        DeviceGuard g(h->device);
+        cudaStream_t st = S(stream);
+        kivi_status rc = ensure_capacity(h, h->l + 1, st);
+        if (rc) return rc;
+        rc = append_launch(h, t_k, t_v, st, QStage{q_src, const_cast<float*>(t_q), q_per_kv});
+        if (rc) return rc;
+        append_bookkeeping(h);
+        return kivi_attend(h, t_q, q_per_kv, out, weights, scale_logits, stream);
+    }
     if (small_fused_ok(h, q_per_kv) && fast_supported(h, q_per_kv) && aligned) {
         DeviceGuard g(h->device);
         cudaStream_t st = S(stream);
@@ -1606,15 +1644,19 @@ kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers,
             const float* dk = zero_copy ? mapped(t_k) : nullptr;
             const float* dv = zero_copy ? mapped(t_v) : nullptr;
             float* dout = zero_copy ? const_cast<float*>(mapped(out)) : nullptr;
-            KIVI_CUDA(cudaMemcpyAsync(sg.q, t_q, sizeof(float) * qrow, cudaMemcpyHostToDevice, st));
+            const float* dq = zero_copy ? mapped(t_q) : nullptr;
+            if (!dq)
+                KIVI_CUDA(cudaMemcpyAsync(sg.q, t_q, sizeof(float) * qrow, cudaMemcpyHostToDevice, st));
             if (!dk || !dv) {
                 KIVI_CUDA(cudaMemcpyAsync(sg.k, t_k, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
                 KIVI_CUDA(cudaMemcpyAsync(sg.v, t_v, sizeof(float) * krow, cudaMemcpyHostToDevice, st));
                 dk = sg.k;
                 dv = sg.v;
             }
-            kivi_status r = kivi_decode(caches[0], sg.q, dk, dv, q_per_kv, dout ? dout : sg.out,
-                                        nullptr, scale_logits, stream);
+            // q is read by every attend item: the append warps stage it from
+            // the mapped host rows into device memory (no copy-engine call)
+            kivi_status r = decode_impl(caches[0], sg.q, dk, dv, q_per_kv, dout ? dout : sg.out,
+                                        nullptr, scale_logits, stream, dq);
             if (r) return r;
             if (!dout)
                 KIVI_CUDA(cudaMemcpyAsync(out, sg.out, sizeof(float) * qrow, cudaMemcpyDeviceToHost, st));
@@ -1658,9 +1700,11 @@ kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers,
         bool warm = true;
         for (int32_t i = 0; i < n_layers; ++i) warm &= caches[i]->part_o != nullptr;
         if (warm) {
-            std::vector<int64_t> l0(n_layers), kc(n_layers), vc(n_layers), ws(n_layers);
+            std::vector<int64_t> l0(n_layers), kc(n_layers), vc(n_layers), ws(n_layers),
+                kq(n_layers);
             for (int32_t i = 0; i < n_layers; ++i) {
                 l0[i] = caches[i]->l;
+                kq[i] = caches[i]->kq_done;
                 kc[i] = caches[i]->kres_cap;
                 vc[i] = caches[i]->vres_cap;
                 ws[i] = caches[i]->work_seq;
@@ -1699,6 +1743,7 @@ kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers,
             sg.graph_capture_failed++;
             for (int32_t i = 0; i < n_layers; ++i) {
                 caches[i]->l = l0[i];
+                caches[i]->kq_done = kq[i];
                 caches[i]->kres_cap = kc[i];
                 caches[i]->vres_cap = vc[i];
                 caches[i]->work_seq = ws[i];
@@ -1918,10 +1963,10 @@ kivi_status kivi_proj_append(kivi_proj* p, kivi_cache* h, const float* x, int64_
         const unsigned fgrid = (unsigned)ceil_div(groups, 256);
         if (cf.bits == 2)
             append_flush_fast_kernel<2><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0,
-                                                              tl0, ntl);
+                                                              tl0, ntl, QStage{nullptr, nullptr, 0});
         else
             append_flush_fast_kernel<4><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0,
-                                                              tl0, ntl);
+                                                              tl0, ntl, QStage{nullptr, nullptr, 0});
         KIVI_LAUNCHED();
         h->total_launches++;
     }
