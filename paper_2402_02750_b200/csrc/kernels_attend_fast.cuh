@@ -622,8 +622,24 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
         if (lane == 0) v = atomicAdd(a.work, 1);
         return __shfl_sync(0xffffffffu, v, 0);
     };
+    // a.prefetch: L2 bulk prefetch of the whole item after next (its 4 x 8 KB
+    // of codes and pairs) as soon as it is grabbed, one item ahead of its TMA
+    // loads: more HBM bytes in flight per SM than the two 8 KB slots per warp
+    auto prefetch_item = [&](int it) {
+        if (!a.prefetch || it >= a.n_items || lane != 0) return;
+        const int pu = it / nper, pk = a.k_first + (it - pu * nper);
+        constexpr int TPI = BSUB / 32;  // key tiles per item
+        bulk_prefetch_l2(c.kcodes + pu * c.k_ustride + (int64_t)pk * TPI * PB::TILE_CODE,
+                         TPI * PB::TILE_CODE);
+        bulk_prefetch_l2(c.kpairs + pu * c.kp_ustride + (int64_t)pk * TPI * D, TPI * D * 8);
+        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * BSUB * PB::TOK_CODE,
+                         BSUB * PB::TOK_CODE);
+        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * BSUB * (D / G),
+                         BSUB * (D / G) * 8);
+    };
     int f_item = grab(), f_job = 0;
     int f_ahead = grab();   // the item after f_item (atomic latency off the critical path)
+    prefetch_item(f_ahead);
     int c_next = f_item;    // next item for the compute loop
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
     auto issue_next = [&](int s) {
@@ -657,7 +673,10 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             f_job = 0;
             f_item = f_ahead;
             c_next = f_item;
-            if (f_item < a.n_items) f_ahead = grab();
+            if (f_item < a.n_items) {
+                f_ahead = grab();
+                prefetch_item(f_ahead);
+            }
             f_u = f_item / nper;
             f_k = f_item - f_u * nper;
         }

@@ -582,8 +582,25 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
         if (lane == 0) v = atomicAdd(a.work, 1);
         return __shfl_sync(FULL, v, 0);
     };
+    // a.prefetch: L2 bulk prefetch of the item after next as soon as it is
+    // grabbed (its 4 x 8 KB of codes and pairs; a partial item's tail too)
+    auto prefetch_item = [&](int it) {
+        if (!a.prefetch || it >= a.n_items || lane != 0) return;
+        const int pu = it / nper, pkk = it - pu * nper, pk = a.k_first + pkk;
+        const int Ti = min(SUB, a.body_end - pkk * SUB);
+        if (Ti <= 0) return;
+        bulk_prefetch_l2(c.kcodes + pu * c.k_ustride + (int64_t)pk * (SUB / 32) * PB::TILE_CODE,
+                         (uint32_t)(Ti / 32) * PB::TILE_CODE);
+        bulk_prefetch_l2(c.kpairs + pu * c.kp_ustride + (int64_t)pk * (SUB / 32) * D,
+                         (uint32_t)(Ti / 32) * D * 8);
+        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * SUB * PB::TOK_CODE,
+                         (uint32_t)Ti * PB::TOK_CODE);
+        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * SUB * (D / fast::G),
+                         (uint32_t)Ti * (D / fast::G) * 8);
+    };
     int f_item = grab(), f_job = 0;
     int f_ahead = grab();
+    prefetch_item(f_ahead);
     int c_next = f_item;
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
     auto issue_next = [&](int s) {
@@ -627,7 +644,10 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             f_job = 0;
             f_item = f_ahead;
             c_next = f_item;
-            if (f_item < a.n_items) f_ahead = grab();
+            if (f_item < a.n_items) {
+                f_ahead = grab();
+                prefetch_item(f_ahead);
+            }
             f_u = f_item / nper;
             f_k = f_item - f_u * nper;
         }

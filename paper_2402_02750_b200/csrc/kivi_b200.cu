@@ -334,6 +334,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
+    int body_prefetch;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -353,6 +354,7 @@ struct Tuning {
         gqa_partial = env_int("KIVI_GQA_PARTIAL", 1);
         gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
         step_graph = env_int("KIVI_STEP_GRAPH", 0);
+        body_prefetch = env_int("KIVI_BODY_PREFETCH", 0);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -739,6 +741,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.l_app = -1;
         a.k_first = 0;
         a.t_first = 0;
+        a.prefetch = tune().body_prefetch;
         a.sub = fast::BSUB;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
@@ -905,6 +908,7 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         a.body_end = (int)body_end;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
+        a.prefetch = tune().body_prefetch;
         take_work_slot(h, a);
         const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][3],
                                                ceil_div(a.n_items, gqa_tc::WARPS));
