@@ -34,4 +34,34 @@ for args in [(2, 16, 700, 1, "fast"), (4, 8, 700, 1, "fast"), (2, 8, 1100, 4, "f
              (2, 8, 1100, 2, "fast"), (2, 4, 300, 1, "generic"), (2, 4, 383, 1, "fast", 3, "1"),
              (2, 4, 127, 4, "fast")]:
     print(args, run(*args), flush=True)
+# projection on tcgen05 fused with the append (K8), across a key-tile boundary
+hin, H, B = 256, 2, 3
+c = kb.KVCache(kb.CacheConfig(2, 32, 128, 128), B * H)
+Kp = torch.rand((B * H, 95, 128), device=dev, generator=g) * 2 - 1
+c.prefill(Kp, Kp)
+W = [torch.randn((hin, H * 128), device=dev, generator=g) / hin ** 0.5 for _ in range(3)]
+p = kb.Projection(*W)
+for _ in range(3):
+    x = torch.randn((B, hin), device=dev, generator=g)
+    q = p.append(c, x)
+    out = c.attend(q)
+p.gemm(torch.randn((5, hin), device=dev, generator=g))
+torch.cuda.synchronize()
+print("projection", float(out.abs().sum()), flush=True)
+p.close()
+c.close()
+
+# single-layer host step: k / v read from mapped pinned memory, q staged by the
+# append warps (QStage), outputs written back across PCIe
+U = 8
+c = kb.KVCache(kb.CacheConfig(2, 32, 128, 128), U)
+Kh = torch.rand((U, 300, 128), device=dev, generator=g)
+c.prefill(Kh, Kh)
+st = kb.LayerStack([c])
+hq, hk, hv, ho = (torch.rand(sh).pin_memory() for sh in ((1, U, 1, 128), (1, U, 128), (1, U, 128),
+                                                         (1, U, 1, 128)))
+for _ in range(3):
+    st.decode_host(hq, hk, hv, ho)
+print("host step", float(ho.abs().sum()), flush=True)
+c.close()
 print("sanitize run done")
