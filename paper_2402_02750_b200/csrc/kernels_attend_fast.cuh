@@ -1088,6 +1088,44 @@ __device__ __forceinline__ void combine_row(const float* __restrict__ part_o,
     if (stat && c == 0) *stat = make_float2(M, L);
 }
 
+// The same merge by ONE warp per row (rows = unit x head): lane owns channels
+// 4*lane .. 4*lane+3 (one float4 per partial: a coalesced 512 B per warp and
+// k), each partial's weight computed once by lane k % 32 and broadcast, the
+// partial loads unrolled 8 deep; no block barriers.  Partial k of the row at
+// ml0 + k * ms.
+__device__ __forceinline__ void combine_row_warp(const float* __restrict__ part_o,
+                                                 const float2* __restrict__ part_ml, int n_sub,
+                                                 int64_t ml0, int ms, float* __restrict__ out_row,
+                                                 float2* __restrict__ stat, int lane) {
+    float M = -INFINITY;
+    for (int k = lane; k < n_sub; k += 32) M = fmaxf(M, __ldcg(&part_ml[ml0 + (int64_t)k * ms]).x);
+    M = warp_max_redux(M);
+    float L = 0.f;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < n_sub; k0 += 32) {
+        float w = 0.f;
+        if (k0 + lane < n_sub) {
+            const float2 m = __ldcg(&part_ml[ml0 + (int64_t)(k0 + lane) * ms]);
+            w = exp2f(m.x - M);
+            L = fmaf(m.y, w, L);
+        }
+        const int nk = min(32, n_sub - k0);
+#pragma unroll 8
+        for (int i = 0; i < nk; ++i) {
+            const float wi = __shfl_sync(0xffffffffu, w, i);
+            const float4 p = __ldcg(reinterpret_cast<const float4*>(
+                                        part_o + (ml0 + (int64_t)(k0 + i) * ms) * D) + lane);
+            o.x = fmaf(p.x, wi, o.x);
+            o.y = fmaf(p.y, wi, o.y);
+            o.z = fmaf(p.z, wi, o.z);
+            o.w = fmaf(p.w, wi, o.w);
+        }
+    }
+    L = warp_sum(L);
+    reinterpret_cast<float4*>(out_row)[lane] = make_float4(o.x / L, o.y / L, o.z / L, o.w / L);
+    if (stat && lane == 0) *stat = make_float2(M, L);
+}
+
 // The same merge as one serial loop per thread: better when there are many
 // rows (thousands of blocks hide each block's latency chain; measured C3 20.5
 // vs 28.5 us), worse when there are few (C1: 12.8 vs 7.4 us).
@@ -1114,8 +1152,16 @@ __device__ __forceinline__ void combine_row_serial(const float* __restrict__ par
 __global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ part_o,
                                                       const float2* __restrict__ part_ml, int n_sub,
                                                       float* __restrict__ out,
-                                                      float2* __restrict__ stats, int parallel) {
+                                                      float2* __restrict__ stats, int parallel,
+                                                      int64_t n_rows) {
     pdl_wait();
+    if (parallel == 2) {  // one warp per unit, four units per block
+        const int64_t u = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+        if (u < n_rows)
+            combine_row_warp(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D,
+                             stats ? stats + u : nullptr, threadIdx.x & 31);
+        return;
+    }
     const int64_t u = blockIdx.x;
     if (parallel)
         combine_row(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D, stats ? stats + u : nullptr);

@@ -498,7 +498,14 @@ __global__ void __launch_bounds__(128) combine_heads_kernel(const float* __restr
                                                             int n_sub, int H,
                                                             float* __restrict__ out,
                                                             float2* __restrict__ stats,
-                                                            int parallel) {
+                                                            int parallel, int64_t n_rows) {
+    if (parallel == 2) {  // one warp per row, four rows per block
+        const int64_t r = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+        if (r < n_rows)
+            fast::combine_row_warp(part_o, part_ml, n_sub, (r / H) * n_sub * H + r % H, H,
+                                   out + r * D, stats ? stats + r : nullptr, threadIdx.x & 31);
+        return;
+    }
     const int64_t r = blockIdx.x;
     const int64_t u = r / H, h = r % H;
     if (parallel)

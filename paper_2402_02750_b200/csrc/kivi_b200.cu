@@ -341,7 +341,7 @@ struct Tuning {
         small_items = env_int("KIVI_SMALL_ITEMS", 1);
         small_fused = env_int("KIVI_SMALL_FUSED", 0);
         small_sub = env_int("KIVI_SMALL_SUB", 0);
-        combine_parallel = env_int("KIVI_COMBINE_PARALLEL", 1);
+        combine_parallel = env_int("KIVI_COMBINE_PARALLEL", -1);
         tail_sub = env_int("KIVI_TAIL_SUB", 256);
         res_sub = env_int("KIVI_RES_SUB", 32);
         res_sub_body = env_int("KIVI_RES_SUB_BODY", 0);
@@ -516,10 +516,14 @@ static void take_work_slot(kivi_cache* h, fast::FastArgs& a) {
 // partials L2-resident after the attend (C1 7.4 vs 12.8 us, C2 8.9 vs 10.0,
 // C3 17.7 vs 21.8, C5 13.2 vs 20.7 us per layer); KIVI_COMBINE_PARALLEL=0
 // selects the serial per-channel merge.
+// K5 merge mode: 0 one serial loop per thread, 1 block-parallel over the
+// partials, 2 one warp per row (KIVI_COMBINE_PARALLEL).
+// Default (-1): warp per row from 4096 rows (C3: +0.6 % per step; C2, 2048
+// rows: neutral; C1, 32 rows: 14 % slower), block-parallel below.
 static int combine_parallel(int64_t rows) {
     const int force = tune().combine_parallel;
-    (void)rows;
-    return force ? 1 : 0;
+    if (force >= 0) return force;
+    return rows >= 4096 ? 2 : 1;
 }
 
 // Launch with programmatic stream serialization (kernel must pdl_wait()
@@ -787,14 +791,16 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     }
     // K5: merge the per-item partials (a separate launch keeps the merge work
     // balanced; fusing it into the attend tail serialised it on the last warps)
+    const int cmode = combine_parallel(U);
+    const unsigned cgrid = (unsigned)(cmode == 2 ? ceil_div(U, 4) : U);
     if (use_pdl && ((nfull == 0 && !h->prof_now) || (one_stream && !h->prof_now)))
-        KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)U), dim3(fast::D), 0, st,
+        KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3(cgrid), dim3(fast::D), 0, st,
                              (const float*)h->part_o, (const float2*)h->part_ml, (int)n_sub, out,
-                             weights ? h->stats : (float2*)nullptr, combine_parallel(U)));
+                             weights ? h->stats : (float2*)nullptr, cmode, (int64_t)U));
     else
-        fast::combine_kernel<<<(unsigned)U, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub,
-                                                              out, weights ? h->stats : nullptr,
-                                                              combine_parallel(U));
+        fast::combine_kernel<<<cgrid, fast::D, 0, st>>>(h->part_o, h->part_ml, (int)n_sub, out,
+                                                        weights ? h->stats : nullptr, cmode,
+                                                        (int64_t)U);
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {
@@ -922,9 +928,10 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         h->events.emplace_back(e0, e1);
         h->main_launches++;
     }
-    gqa::combine_heads_kernel<<<(unsigned)(U * H), fast::D, 0, st>>>(
-        h->part_o, h->part_ml, (int)n_parts, H, out, weights ? h->stats : nullptr,
-        combine_parallel(U * H));
+    const int cmode = combine_parallel(U * H);
+    gqa::combine_heads_kernel<<<(unsigned)(cmode == 2 ? ceil_div(U * H, 4) : U * H), fast::D, 0,
+                                st>>>(h->part_o, h->part_ml, (int)n_parts, H, out,
+                                      weights ? h->stats : nullptr, cmode, (int64_t)(U * H));
     KIVI_LAUNCHED();
     h->total_launches++;
     if (weights) {

@@ -313,6 +313,39 @@ def test_decode_fast_vs_reference(cuda, bits, l0, route, monkeypatch):
     assert e_w <= 1e-5, e_w
 
 
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("qpk", [1, 4])
+def test_combine_modes(cuda, mode, qpk, monkeypatch):
+    """Every K5 merge mode (serial per thread, block-parallel, one warp per row)
+    against the reference, MHA and GQA, with weights (the merge's (M, L) stats)."""
+    monkeypatch.setenv("KIVI_COMBINE_PARALLEL", mode)
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", "0")
+    ck = checker()
+    rng = np.random.default_rng(17 + qpk + int(mode))
+    U, l0, d = 5, 1300, 128
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    cache = kb.KVCache(kb.CacheConfig(2, 32, 128, d), U)
+    cache.prefill(dev(K), dev(V))
+    refs = [[ck.unit(2, 32, 128, d) for _ in range(qpk)] for _ in range(U)]
+    for u in range(U):
+        for r in refs[u]:
+            r.prefill(K[u], V[u])
+    for step in range(3):
+        q = rnd(rng, U, qpk, d)
+        tk, tv = rnd(rng, U, d), rnd(rng, U, d)
+        use_w = step == 2
+        res = cache.decode(dev(q), dev(tk), dev(tv), q_per_kv=qpk, weights=use_w)
+        out, w = res if use_w else (res, None)
+        out = out.cpu().numpy()
+        for u in range(U):
+            for h in range(qpk):
+                ro, rw = refs[u][h].decode(q[u, h], tk[u], tv[u], weights=True)
+                assert rel_l2(out[u, h], ro) <= 1e-5, f"mode {mode} step {step} unit {u} head {h}"
+                if use_w:
+                    assert float(np.max(np.abs(w[u, h].cpu().numpy() - rw))) <= 1e-5
+    cache.close()
+
+
 @pytest.mark.parametrize("small", ["0", "1"])
 @pytest.mark.parametrize("qpk", [1, 4])
 def test_layers_interleaved_on_one_stream(cuda, small, qpk, monkeypatch):
