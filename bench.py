@@ -642,8 +642,9 @@ def run_ours(args):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("config") == args.config and tj.get("bits") == bits:
-                traffic = tj.get("dram_bytes_per_launch")
+            ent = tj.get("configs", {}).get(f"{args.config}/{bits}")
+            if ent:
+                traffic = ent.get("dram_bytes_per_launch")
         except Exception:
             pass
 
