@@ -4,6 +4,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Persistent attend kernels: claim the item after next with the current
+// item's first job and broadcast it one item later (1), or claim and
+// broadcast at once (0, default: 1 measured 0.5-1 % slower on C2 / C3
+// although the broadcast shuffle was the body's most-stalled instruction).
+#ifndef KIVI_DEFER_CLAIM
+#define KIVI_DEFER_CLAIM 0
+#endif
+
 namespace kivi_b200 {
 
 // ---------------------------------------------------------------------------

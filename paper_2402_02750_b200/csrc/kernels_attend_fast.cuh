@@ -640,11 +640,17 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     int f_item = grab(), f_job = 0;
     int f_ahead = grab();   // the item after f_item (atomic latency off the critical path)
     prefetch_item(f_ahead);
+    // The claim of the item after f_ahead is issued with f_item's first job
+    // and read (broadcast from lane 0) only when f_item's jobs are all issued:
+    // the atomic's round trip overlaps a whole item instead of stalling the
+    // warp at the broadcast.
+    int pend = 0;
     int c_next = f_item;    // next item for the compute loop
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
+            if (KIVI_DEFER_CLAIM && f_job == 0 && f_ahead < a.n_items) pend = atomicAdd(a.work, 1);
             uint8_t* slot = wbase + s * SLOT;
             uint64_t* bar = &bars[s];
             fence_proxy_async_smem();
@@ -674,7 +680,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             f_item = f_ahead;
             c_next = f_item;
             if (f_item < a.n_items) {
-                f_ahead = grab();
+                f_ahead = KIVI_DEFER_CLAIM ? __shfl_sync(0xffffffffu, pend, 0) : grab();
                 prefetch_item(f_ahead);
             }
             f_u = f_item / nper;

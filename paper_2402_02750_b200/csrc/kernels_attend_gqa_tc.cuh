@@ -601,11 +601,17 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     int f_item = grab(), f_job = 0;
     int f_ahead = grab();
     prefetch_item(f_ahead);
+    // The claim of the item after f_ahead is issued with f_item's first job
+    // and read (broadcast from lane 0) only when f_item's jobs are all issued:
+    // the atomic's round trip overlaps a whole item instead of stalling the
+    // warp at the broadcast.
+    int pend = 0;
     int c_next = f_item;
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
+            if (KIVI_DEFER_CLAIM && f_job == 0 && f_ahead < a.n_items) pend = atomicAdd(a.work, 1);
             uint8_t* slot = wbase + s * SLOT;
             uint64_t* bar = &bars[s];
             const int kk = a.k_first + f_k;
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             f_item = f_ahead;
             c_next = f_item;
             if (f_item < a.n_items) {
-                f_ahead = grab();
+                f_ahead = KIVI_DEFER_CLAIM ? __shfl_sync(0xffffffffu, pend, 0) : grab();
                 prefetch_item(f_ahead);
             }
             f_u = f_item / nper;
