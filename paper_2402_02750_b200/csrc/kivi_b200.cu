@@ -347,7 +347,7 @@ struct Tuning {
         res_sub_body = env_int("KIVI_RES_SUB_BODY", 0);
         mha_tc = env_int("KIVI_MHA_TC", 0);
         pdl = env_int("KIVI_PDL", 1);
-        tail_ctas = env_int("KIVI_TAIL_CTAS", 2);
+        tail_ctas = env_int("KIVI_TAIL_CTAS", 1);
         tail_warp_ctas = env_int("KIVI_TAIL_WARP_CTAS", 0);
         tail_last = env_int("KIVI_TAIL_LAST", 0);
         gqa_tc = env_int("KIVI_GQA_TC", 1);
