@@ -242,12 +242,12 @@ using WS2 = WarpSmem<2>;
 // then only the last value job still reads p, and it reads tokens
 // >= BSUB - VQ_TOK >= 128 (NVJ >= 2).  Keeps 3 CTAs x 4 warps per SM.
 // (VI, the tensor-core value jobs, keeps their B digits in the job's slot.)
-template <bool VI = false>
+template <bool VI = false, int BS = BSUB>
 struct WarpSmemBody {
     static constexpr int QQ_OFF = 2 * SLOT;
     static constexpr int PROBS_OFF = QQ_OFF + D * 4;
     static constexpr int QRAW_OFF = PROBS_OFF;
-    static constexpr int BAR_OFF = PROBS_OFF + BSUB * 4;
+    static constexpr int BAR_OFF = PROBS_OFF + BS * 4;
     static constexpr int BYTES = BAR_OFF + 16;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
 };
@@ -585,14 +585,16 @@ __device__ __forceinline__ void v_finalize(uint8_t* slot, const float2* vacc, fl
 // and value are quantized, so the job sequence is fixed (B=2: 2 key jobs of 4
 // tiles, 2 value jobs of 128 tokens) and the issue path is straight-line.
 // VI (B = 2 only): P.V on the integer tensor cores (kernels_vimma.cuh).
-template <int B, bool VI = false>
+// BS: tokens per item (BSUB = 256 by default; 512 for long contexts, where
+// the residual region it widens is a small share: C5 +1.7 %, C2 -5 %).
+template <int B, bool VI = false, int BS = BSUB>
 __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) {
     using PB = P<B>;
-    using WSB = WarpSmemBody<VI>;
+    using WSB = WarpSmemBody<VI, BS>;
     static_assert(!VI || B == 2, "tensor-core value jobs: 2-bit codes");
-    constexpr int NKJ = (BSUB / 32) / PB::KQ_TILES;  // key jobs per item
-    constexpr int NVJ = BSUB / PB::VQ_TOK;           // value jobs per item
-    static_assert(NVJ >= 2 && BSUB - PB::VQ_TOK >= D, "q staging aliases p[0..127]");
+    constexpr int NKJ = (BS / 32) / PB::KQ_TILES;  // key jobs per item
+    constexpr int NVJ = BS / PB::VQ_TOK;           // value jobs per item
+    static_assert(NVJ >= 2 && BS - PB::VQ_TOK >= D, "q staging aliases p[0..127]");
     constexpr int NJ = NKJ + NVJ;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -628,14 +630,14 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     auto prefetch_item = [&](int it) {
         if (!a.prefetch || it >= a.n_items || lane != 0) return;
         const int pu = it / nper, pk = a.k_first + (it - pu * nper);
-        constexpr int TPI = BSUB / 32;  // key tiles per item
+        constexpr int TPI = BS / 32;  // key tiles per item
         bulk_prefetch_l2(c.kcodes + pu * c.k_ustride + (int64_t)pk * TPI * PB::TILE_CODE,
                          TPI * PB::TILE_CODE);
         bulk_prefetch_l2(c.kpairs + pu * c.kp_ustride + (int64_t)pk * TPI * D, TPI * D * 8);
-        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * BSUB * PB::TOK_CODE,
-                         BSUB * PB::TOK_CODE);
-        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * BSUB * (D / G),
-                         BSUB * (D / G) * 8);
+        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * BS * PB::TOK_CODE,
+                         BS * PB::TOK_CODE);
+        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * BS * (D / G),
+                         BS * (D / G) * 8);
     };
     int f_item = grab(), f_job = 0;
     int f_ahead = grab();   // the item after f_item (atomic latency off the critical path)
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             uint64_t* bar = &bars[s];
             fence_proxy_async_smem();
             if (f_job < NKJ) {
-                const int64_t tile0 = (int64_t)f_k * (BSUB / 32) + f_job * PB::KQ_TILES;
+                const int64_t tile0 = (int64_t)f_k * (BS / 32) + f_job * PB::KQ_TILES;
                 constexpr uint32_t cb = PB::KQ_TILES * PB::TILE_CODE;
                 constexpr uint32_t pb = PB::KQ_TILES * D * 8;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? D * 4 : 0));
@@ -665,7 +667,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
                                      policy);
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * D, D * 4, bar);
             } else {
-                const int64_t ts = (int64_t)f_k * BSUB + (f_job - NKJ) * PB::VQ_TOK;
+                const int64_t ts = (int64_t)f_k * BS + (f_job - NKJ) * PB::VQ_TOK;
                 constexpr uint32_t cb = PB::VQ_TOK * PB::TOK_CODE;
                 constexpr uint32_t pb = PB::VQ_TOK * (D / G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
@@ -715,7 +717,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             release_slot();
         }
         const float2 ml = softmax_item(
-            probs, BSUB, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * BSUB : nullptr, lane);
+            probs, BS, a.wlog ? a.wlog + (int64_t)u * a.l + (int64_t)k * BS : nullptr, lane);
         if constexpr (VI) {
             vimma::State st;
             vimma::begin_item(st);

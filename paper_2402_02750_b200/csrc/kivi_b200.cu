@@ -124,7 +124,8 @@ struct kivi_cache {
     int64_t scratch_cap = 0;
     float2* stats = nullptr;
     int64_t stats_cap = 0;
-    int fast_per_sm[9][5] = {};  // [B][body, tail, gqa_tc, small_fused, body_vimma]
+    // [B][body, tail, gqa_tc, small_fused, body_vimma, body 512, body_vimma 512]
+    int fast_per_sm[9][7] = {};
     // staging for _host calls
     // host-path staging, double-buffered: call i uploads into stg[i & 1]
     // while call i-1's kernels may still read stg[(i-1) & 1]
@@ -334,7 +335,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
-    int body_prefetch;
+    int body_prefetch, body_long_l;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -355,6 +356,7 @@ struct Tuning {
         gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
         step_graph = env_int("KIVI_STEP_GRAPH", 0);
         body_prefetch = env_int("KIVI_BODY_PREFETCH", 0);
+        body_long_l = env_int("KIVI_BODY_LONG_L", 16384);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -575,10 +577,14 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // fused append: the body must not cover the token the append pops into the
     // quantized store (token vg - 1), so it stops at floor32(vg - 1)
     const int64_t body_vg = l_app >= 0 ? h->vg() - 1 : h->vg();
-    const int64_t nfull = latency_bound ? 0 : ((body_vg / 32) * 32) / fast::BSUB;
+    // body item size: 512 tokens from KIVI_BODY_LONG_L tokens (default 16384;
+    // 0 disables), where the wider residual region is a small share
+    const int long_l = tune().body_long_l;
+    const int bsub = (long_l > 0 && h->l >= long_l && l_app < 0 && !tune().mha_tc) ? 512 : fast::BSUB;
+    const int64_t nfull = latency_bound ? 0 : ((body_vg / 32) * 32) / bsub;
     if (l_app >= 0 && (latency_bound || nfull == 0))
         return fail(KIVI_ERR_USAGE, "internal: fused append outside its route");
-    const int64_t t_first = nfull * fast::BSUB;
+    const int64_t t_first = nfull * bsub;
     const int tsub = latency_bound ? tsub_small : tsub_env;
     // few-unit route: the residual window [floor32(vg), l) in rsub-token items
     const int rsub_env = tune().res_sub / 32 * 32;
@@ -620,10 +626,16 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int smem = fast::WS2::STRIDE * fast::WARPS;
     // P.V of the body on the integer tensor cores (2-bit; kernels_vimma.cuh)
     const bool vimma = B == 2 && tune().vimma;
-    const int smem_body = (vimma ? fast::WarpSmemBody<true>::STRIDE : fast::WSB::STRIDE) * fast::WARPS;
-    void (*body_kernel)(fast::FastArgs) = fast::attend_body_kernel<B>;
+    const bool b512 = bsub == 512;
+    const int smem_body =
+        (b512 ? (vimma ? fast::WarpSmemBody<true, 512>::STRIDE : fast::WarpSmemBody<false, 512>::STRIDE)
+              : (vimma ? fast::WarpSmemBody<true>::STRIDE : fast::WSB::STRIDE)) *
+        fast::WARPS;
+    void (*body_kernel)(fast::FastArgs) =
+        b512 ? fast::attend_body_kernel<B, false, 512> : fast::attend_body_kernel<B>;
     if constexpr (B == 2)
-        if (vimma) body_kernel = fast::attend_body_kernel<2, true>;
+        if (vimma)
+            body_kernel = b512 ? fast::attend_body_kernel<2, true, 512> : fast::attend_body_kernel<2, true>;
     const int smem_tc = gqa_tc::TS<1>::STRIDE * gqa_tc::WARPS;
     const int mha_tc = tune().mha_tc;  // measured slower on C2
     if (h->fast_per_sm[B][0] == 0) {
@@ -654,6 +666,20 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &per_sm, fast::attend_body_kernel<2, true>, fast::WARPS * 32, smem_vi));
             h->fast_per_sm[B][4] = per_sm < 1 ? 1 : per_sm;
+            const int smem_vi5 = fast::WarpSmemBody<true, 512>::STRIDE * fast::WARPS;
+            KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<2, true, 512>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_vi5));
+            KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, fast::attend_body_kernel<2, true, 512>, fast::WARPS * 32, smem_vi5));
+            h->fast_per_sm[B][6] = per_sm < 1 ? 1 : per_sm;
+        }
+        {
+            const int smem5 = fast::WarpSmemBody<false, 512>::STRIDE * fast::WARPS;
+            KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<B, false, 512>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem5));
+            KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, fast::attend_body_kernel<B, false, 512>, fast::WARPS * 32, smem5));
+            h->fast_per_sm[B][5] = per_sm < 1 ? 1 : per_sm;
         }
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
@@ -746,21 +772,22 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
         a.k_first = 0;
         a.t_first = 0;
         a.prefetch = tune().body_prefetch;
-        a.sub = fast::BSUB;
+        a.sub = bsub;
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
         take_work_slot(h, a);
-        if (B == 2 && mha_tc && fast::BSUB == fast::SUB) {
+        if (B == 2 && mha_tc && bsub == fast::SUB) {
             // tensor-core body (kernels_attend_gqa_tc.cuh with one query head):
             // every item is a whole SUB-token sub-chunk below nfull * BSUB
-            a.body_end = (int)(nfull * fast::BSUB);
+            a.body_end = (int)(nfull * bsub);
             const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[B][2],
                                                    ceil_div(a.n_items, gqa_tc::WARPS));
             gqa_tc::attend_gqa_tc_kernel<1>
                 <<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
         } else {
             const int64_t grid = std::min<int64_t>(
-                (int64_t)num_sms() * h->fast_per_sm[B][vimma ? 4 : 0], ceil_div(a.n_items, fast::WARPS));
+                (int64_t)num_sms() * h->fast_per_sm[B][b512 ? (vimma ? 6 : 5) : (vimma ? 4 : 0)],
+                ceil_div(a.n_items, fast::WARPS));
             if (tail_deferred) {
                 // body first (normal launch: the append is complete), then the
                 // residual-window kernel as its programmatic dependent
