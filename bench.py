@@ -148,6 +148,17 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def clocks_bad(cs):
+    """A timed region's clock summary that rejects the measurement: a hardware
+    or thermal slowdown, or SM clocks stuck well below max with no reason (a
+    leftover clock lock).  sw_power_cap is kept (noted in the line)."""
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if set(cs.get("reasons") or []) & bad:
+        return True
+    mhz, mx = cs.get("sm_mhz"), cs.get("sm_max_mhz")
+    return bool(mhz and mx and mhz < 0.75 * mx and not cs.get("reasons"))
+
+
 def attend_kernel_name(qpk, units, ctx, sms=148):
     """The attend launch the roofline times (library routing, kivi_b200.cu)."""
     if qpk > 1:
@@ -492,14 +503,6 @@ def run_ours(args):
     # well below max with no reason (a leftover clock lock), is re-measured
     # once (any rank's verdict applies to all); the first attempt is reported.
     remeasured = None
-
-    def clocks_bad(cs):
-        bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
-        if set(cs.get("reasons") or []) & bad:
-            return True
-        mhz, mx = cs.get("sm_mhz"), cs.get("sm_max_mhz")
-        return bool(mhz and mx and mhz < 0.75 * mx and not cs.get("reasons"))
-
     if max_over_ranks(float(clocks_bad(clocks.summary()))) > 0:
         remeasured = {"first_value": global_batch * steps / elapsed,
                       "first_clocks": clocks.summary()}

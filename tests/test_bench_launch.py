@@ -57,3 +57,19 @@ def test_reference_arm_config_matches_ours():
     c1, u1, s1 = bench.workload_config(a, 1, 0, None)
     c2, u2, s2 = bench.workload_config(a, 1, 0, 180e9)
     assert c1 == c2 and u1 == u2 == 2048 and s1 == s2 == "weak"
+
+
+def test_clock_rejection_rule():
+    """bench.py re-measures once when the timed region saw a hardware / thermal
+    slowdown or clocks stuck well below max with no reason; a power cap is kept."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    ok = {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": []}
+    assert not bench.clocks_bad(ok)
+    assert not bench.clocks_bad(dict(ok, sm_mhz=1700, reasons=["sw_power_cap"]))
+    assert bench.clocks_bad(dict(ok, reasons=["hw_slowdown"]))
+    assert bench.clocks_bad(dict(ok, reasons=["sw_power_cap", "sw_thermal_slowdown"]))
+    assert bench.clocks_bad(dict(ok, sm_mhz=1200))
+    assert not bench.clocks_bad({"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]})
