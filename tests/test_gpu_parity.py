@@ -240,6 +240,35 @@ def test_prefill_unaligned_rows(cuda):
     cache.close()
 
 
+@pytest.mark.parametrize("bits", [2, 4])
+def test_long_stream_many_flushes(cuda, bits, monkeypatch):
+    """1,100 appends from l = 301 (9 key flushes, 36 early key-tile quantisations,
+    1,100 value pops) on the fast kernels, decoding every step: outputs within
+    1e-5 of the reference at every step and the state bit-identical at every
+    flush boundary -- no drift between the device store and the reference's."""
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", "0")
+    ck = checker()
+    rng = np.random.default_rng(900 + bits)
+    U, d, l0, steps = 4, 128, 301, 1100
+    K, V = rnd(rng, U, l0, d), rnd(rng, U, l0, d)
+    cache = kb.KVCache(kb.CacheConfig(bits, 32, 128, d), U)
+    cache.prefill(dev(K), dev(V))
+    refs = [ck.unit(bits, 32, 128, d) for _ in range(U)]
+    for u in range(U):
+        refs[u].prefill(K[u], V[u])
+    worst = 0.0
+    for s_ in range(steps):
+        q, tk, tv = rnd(rng, U, d), rnd(rng, U, d), rnd(rng, U, d)
+        out = cache.decode(dev(q)[:, None, :].contiguous(), dev(tk), dev(tv)).cpu().numpy()
+        for u in range(U):
+            worst = max(worst, rel_l2(out[u, 0], refs[u].decode(q[u], tk[u], tv[u])))
+        if (l0 + s_ + 1) % 128 == 0:
+            for u in range(U):
+                assert_state_equal(cache.export_unit(u), refs[u].export(), f"l={l0 + s_ + 1} u={u}")
+    assert worst <= 1e-5, worst
+    cache.close()
+
+
 def test_streaming_equals_batch(cuda):
     # reference test_kv_cache.cpp:133-157 on the device path
     rng = np.random.default_rng(25)
