@@ -240,6 +240,15 @@ kivi_status kivi_dequantize_matrix(const uint8_t* packed, const double* zero_poi
                                    const double* scales, int64_t rows, int64_t cols,
                                    int32_t bits, int64_t group_size, kivi_axis axis, float* out,
                                    void* stream);
+/* Reference quantize_group (quantize.cpp:22-48) of one group of n values (any
+ * n >= 1, B in [1, 8]): codes[n] (uint8), *zero_point, *scale as the
+ * reference's doubles; dequantized (NULL or [n] fp32) receives
+ * dequantize_group (quantize.cpp:50-57) of the result.  One launch, all
+ * pointers device-accessible (device or mapped host memory).  Empty group or
+ * B out of range: KIVI_ERR_USAGE (the reference's UsageError). */
+kivi_status kivi_quantize_group(const float* values, int64_t n, int32_t bits, uint8_t* codes,
+                                double* zero_point, double* scale, float* dequantized,
+                                void* stream);
 /* Unpacked-code variants for ANY B in [1, 8] (reference quantize_grouped /
  * dequantize_grouped, quantize.cpp:105-167, used by quantize_group and
  * fake_quantize which accept non-packable B): one uint8 code per element, in

@@ -127,6 +127,7 @@ HEADER_SYMBOLS = {
     "kivi_quantize_matrix": (ctypes.c_int, [P, I64, I64, I32, I64, ctypes.c_int, P, P, P, P]),
     "kivi_dequantize_matrix": (ctypes.c_int, [P, P, P, I64, I64, I32, I64, ctypes.c_int, P, P]),
     "kivi_quantize_codes": (ctypes.c_int, [P, I64, I64, I32, I64, ctypes.c_int, P, P, P, P]),
+    "kivi_quantize_group": (ctypes.c_int, [P, I64, I32, P, P, P, P, P]),
     "kivi_dequantize_codes": (ctypes.c_int, [P, P, P, I64, I64, I64, ctypes.c_int, P, P]),
     "kivi_pack_codes": (ctypes.c_int, [P, I64, I32, P, P]),
     "kivi_unpack_codes": (ctypes.c_int, [P, I64, I32, P, P]),

@@ -487,6 +487,63 @@ __global__ void __launch_bounds__(256) prefill_values_fast_kernel(CacheDev c,
     }
 }
 
+// ---- one group, quantized and dequantized in one launch --------------------
+// Reference quantize_group (quantize.cpp:22-48) of n values (any n, any B in
+// [1, 8]) followed by dequantize_group (quantize.cpp:50-57) of its result: one
+// CTA, every value loaded once in parallel (the facade's inputs sit in mapped
+// host memory: a serial per-value loop would be one PCIe round trip per value),
+// first-smallest / last-largest by index, codes decided exactly as
+// quant_code, z / s as the reference's doubles.
+__global__ void __launch_bounds__(256) quantize_group_kernel(const float* __restrict__ v, int n,
+                                                             int maxc, uint8_t* __restrict__ codes,
+                                                             double* __restrict__ zp,
+                                                             double* __restrict__ sc,
+                                                             float* __restrict__ deq) {
+    __shared__ float s_lo[8], s_hi[8];
+    __shared__ int s_ilo[8], s_ihi[8];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    float lo = INFINITY, hi = -INFINITY;
+    int ilo = INT_MAX, ihi = -1;
+    for (int i = t; i < n; i += blockDim.x) {
+        const float x = v[i];
+        if (x < lo || (!(lo < x) && i < ilo)) { lo = x; ilo = i; }
+        if (x > hi || (!(hi > x) && i > ihi)) { hi = x; ihi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const int oilo = __shfl_xor_sync(0xffffffffu, ilo, o);
+        const float ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const int oihi = __shfl_xor_sync(0xffffffffu, ihi, o);
+        if (olo < lo || (!(lo < olo) && oilo < ilo)) { lo = olo; ilo = oilo; }
+        if (ohi > hi || (!(hi > ohi) && oihi > ihi)) { hi = ohi; ihi = oihi; }
+    }
+    if (lane == 0) {
+        s_lo[warp] = lo; s_ilo[warp] = ilo;
+        s_hi[warp] = hi; s_ihi[warp] = ihi;
+    }
+    __syncthreads();
+    lo = s_lo[0]; ilo = s_ilo[0]; hi = s_hi[0]; ihi = s_ihi[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        if (s_ilo[w] >= 0 && s_ilo[w] != INT_MAX &&
+            (s_lo[w] < lo || (!(lo < s_lo[w]) && s_ilo[w] < ilo))) { lo = s_lo[w]; ilo = s_ilo[w]; }
+        if (s_ihi[w] >= 0 && (s_hi[w] > hi || (!(hi > s_hi[w]) && s_ihi[w] > ihi))) {
+            hi = s_hi[w]; ihi = s_ihi[w];
+        }
+    }
+    // lo / hi are elements of v (the reference's minmax_element values)
+    const CodeCtx cc = make_code_ctx(lo, hi, maxc);
+    const double s = group_scale(lo, hi, maxc);
+    for (int i = t; i < n; i += blockDim.x) {
+        const uint32_t q = hi == lo ? 0u : quant_code(cc, v[i]);
+        codes[i] = (uint8_t)q;
+        if (deq) deq[i] = dequant_exact(q, s, (double)lo);
+    }
+    if (t == 0) {
+        *zp = (double)lo;
+        *sc = s;
+    }
+}
+
 // ---- materialize (reference materialize_*, kv_cache.cpp:100-106) ---------
 __global__ void materialize_kernel(CacheDev c, int64_t l, int64_t kg, int64_t vg,
                                    float* __restrict__ kout, float* __restrict__ vout) {

@@ -2239,6 +2239,18 @@ kivi_status kivi_quantize_codes(const float* m, int64_t rows, int64_t cols, int3
     return KIVI_OK;
 }
 
+kivi_status kivi_quantize_group(const float* values, int64_t n, int32_t bits, uint8_t* codes,
+                                double* zero_point, double* scale, float* dequantized,
+                                void* stream) {
+    if (n < 1) return fail(KIVI_ERR_USAGE, "quantize_group: empty group");
+    if (bits < 1 || bits > 8) return fail(KIVI_ERR_USAGE, "quantize_group: bits out of range");
+    if (n >= (1LL << 31)) return fail(KIVI_ERR_SHAPE, "quantize_group: group too large");
+    quantize_group_kernel<<<1, 256, 0, S(stream)>>>(values, (int)n, (1 << bits) - 1, codes,
+                                                    zero_point, scale, dequantized);
+    KIVI_LAUNCHED();
+    return KIVI_OK;
+}
+
 kivi_status kivi_dequantize_codes(const uint8_t* codes, const double* zero_points,
                                   const double* scales, int64_t rows, int64_t cols,
                                   int64_t group_size, kivi_axis axis, float* out, void* stream) {

@@ -570,11 +570,9 @@ GroupQuant quantize_group(std::span<const float> values, int bits) {
     float* din = mapped().dev(reinterpret_cast<float*>(buf));
     std::uint8_t* dbuf = reinterpret_cast<std::uint8_t*>(din);
     double* dz = reinterpret_cast<double*>(dbuf + o_z);
-    check(kivi_quantize_codes(din, 1, (int64_t)n, bits, (int64_t)n, KIVI_PER_TOKEN,
-                              dbuf + o_codes, dz, dz + 1, facade_stream()));
-    check(kivi_dequantize_codes(dbuf + o_codes, dz, dz + 1, 1, (int64_t)n, (int64_t)n,
-                                KIVI_PER_TOKEN, reinterpret_cast<float*>(dbuf + o_deq),
-                                facade_stream()));
+    // one launch: quantize, then dequantize the result (kivi_quantize_group)
+    check(kivi_quantize_group(din, (int64_t)n, bits, dbuf + o_codes, dz, dz + 1,
+                              reinterpret_cast<float*>(dbuf + o_deq), facade_stream()));
     facade_wait(facade_stream());
     GroupQuant g;
     g.codes.assign(buf + o_codes, buf + o_codes + n);

@@ -53,6 +53,7 @@ class Port(_Base):
             L = ctypes.CDLL(PORT_LIB)
             sig = {
                 "oracle_quantize_group": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P]),
+                "oracle_dequantize_group": (None, [P, I64, ctypes.c_double, ctypes.c_double, P]),
                 "oracle_pack_codes": (ctypes.c_int, [P, I64, ctypes.c_int, P]),
                 "oracle_unpack_codes": (ctypes.c_int, [P, I64, I64, ctypes.c_int, P]),
                 "oracle_quantize_matrix": (ctypes.c_int,

@@ -115,6 +115,45 @@ def test_quantize_group_spec_examples(cuda):
         kb.quantize_matrix(dev(rnd(np.random.default_rng(0), 4, 2)), 3, 2, True)
 
 
+@pytest.mark.parametrize("bits", [1, 2, 3, 4, 8])
+def test_quantize_group_single_launch(cuda, bits):
+    """kivi_quantize_group (the facade's quantize_group: one launch that also
+    dequantizes) == the reference's quantize_group + dequantize_group, on group
+    sizes 1..1000 with ties, constants and signed zeros."""
+    import ctypes
+    from oracles import Port
+    rng = np.random.default_rng(50 + bits)
+    cases = [rnd(rng, n) for n in (1, 2, 3, 31, 32, 33, 255, 256, 257, 1000)]
+    cases += [np.full(17, 0.1, np.float32), np.array([0.0, -0.0, 0.5, -0.0], np.float32),
+              np.array([-0.5, -0.0, 0.0, -0.5], np.float32),
+              np.round(rnd(rng, 64) * 2) / 2]
+    lib = kb.lib()
+    port = Port.lib()
+    for v in cases:
+        v = np.ascontiguousarray(v, np.float32)
+        n = v.size
+        dv = dev(v)
+        codes = torch.empty(n, dtype=torch.uint8, device="cuda")
+        zs = torch.empty(2, dtype=torch.float64, device="cuda")
+        deq = torch.empty(n, dtype=torch.float32, device="cuda")
+        st = lib.kivi_quantize_group(dv.data_ptr(), n, bits, codes.data_ptr(), zs.data_ptr(),
+                                     zs.data_ptr() + 8, deq.data_ptr(), None)
+        assert st == 0, lib.kivi_last_error()
+        torch.cuda.synchronize()
+        want_c = np.zeros(n, np.uint8)
+        want_zs = np.zeros(2, np.float64)
+        port.oracle_quantize_group(v.ctypes.data, n, bits, want_c.ctypes.data,
+                                   want_zs.ctypes.data, want_zs[1:].ctypes.data)
+        want_d = np.zeros(n, np.float32)
+        port.oracle_dequantize_group(want_c.ctypes.data, n, ctypes.c_double(want_zs[0]),
+                                     ctypes.c_double(want_zs[1]), want_d.ctypes.data)
+        assert codes.cpu().numpy().tobytes() == want_c.tobytes(), (bits, n)
+        assert zs.cpu().numpy().tobytes() == want_zs.tobytes(), (bits, n)
+        assert deq.cpu().numpy().tobytes() == want_d.tobytes(), (bits, n)
+    assert lib.kivi_quantize_group(dv.data_ptr(), 0, bits, codes.data_ptr(), zs.data_ptr(),
+                                   zs.data_ptr() + 8, None, None) == 2  # KIVI_ERR_USAGE
+
+
 def test_pack_unpack_identity(cuda):
     rng = np.random.default_rng(12)
     for bits in (1, 2, 4, 8):
