@@ -122,6 +122,8 @@ struct kivi_cache {
     int64_t ml_cap = 0;
     float* scratch = nullptr;
     int64_t scratch_cap = 0;
+    float* heads_buf = nullptr;  // per-head GQA route: q / out (/ weights) by head
+    int64_t heads_cap = 0;
     float2* stats = nullptr;
     int64_t stats_cap = 0;
     // [B][body, tail, gqa_tc, small_fused, body_vimma, body 512, body_vimma 512]
@@ -335,7 +337,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
-    int body_prefetch, body_long_l;
+    int body_prefetch, body_long_l, gqa_heads;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -357,6 +359,7 @@ struct Tuning {
         step_graph = env_int("KIVI_STEP_GRAPH", 0);
         body_prefetch = env_int("KIVI_BODY_PREFETCH", 0);
         body_long_l = env_int("KIVI_BODY_LONG_L", 16384);
+        gqa_heads = env_int("KIVI_GQA_HEADS", 1);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -1056,6 +1059,7 @@ kivi_status kivi_cache_destroy(kivi_cache* h) {
     cudaFree(h->part_o);
     cudaFree(h->part_ml);
     cudaFree(h->scratch);
+    cudaFree(h->heads_buf);
     cudaFree(h->stats);
     for (auto& sg : h->stg) {
         cudaFree(sg.q);
@@ -1318,6 +1322,71 @@ kivi_status kivi_append(kivi_cache* h, const float* t_k, const float* t_v, void*
     return KIVI_OK;
 }
 
+extern "C++" {
+namespace {
+// rows of `len` floats: dst row (h, u) <- src row (u, h) (to_heads), or the
+// reverse; one float4 per thread (len % 4 == 0)
+__global__ void permute_heads_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                     int64_t U, int H, int64_t len, int to_heads) {
+    const int64_t v4 = len / 4, total = U * H * v4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / v4, c = i - row * v4;  // row in dst order
+        int64_t srow;
+        if (to_heads) {  // dst (h, u) <- src (u, h)
+            const int64_t hh = row / U, u = row - hh * U;
+            srow = u * H + hh;
+        } else {  // dst (u, h) <- src (h, u)
+            const int64_t u = row / H, hh = row - u * H;
+            srow = hh * U + u;
+        }
+        reinterpret_cast<float4*>(dst)[row * v4 + c] =
+            reinterpret_cast<const float4*>(src)[srow * v4 + c];
+    }
+}
+}  // namespace
+
+// GQA shapes the tensor-core kernel does not cover (B = 4, or q_per_kv not in
+// {2, 4}) but the MHA fast kernels do (d = 128, G = 32, B in {2, 4}): one MHA
+// attend per query head over the shared cache (q_per_kv passes over the
+// bytes -- against the generic kernel's reference-order double loop, ~65x
+// faster at C3's shape in 4 bits).  q and the outputs are permuted to and from
+// head-major rows around the passes.
+template <int B>
+static kivi_status attend_heads_mha(kivi_cache* h, const float* t_q, int qpk, float* out,
+                                    float* weights, float qscale, cudaStream_t st) {
+    const int64_t U = h->n_units, d = h->cfg.head_dim, l = h->l;
+    const int64_t need = 2 * qpk * U * d + (weights ? qpk * U * l : 0);
+    kivi_status rc = ensure(&h->heads_buf, &h->heads_cap, need);
+    if (rc) return rc;
+    float* qh = h->heads_buf;
+    float* oh = qh + qpk * U * d;
+    float* wh = weights ? oh + qpk * U * d : nullptr;
+    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(t_q, qh, U, qpk, d, 1);
+    KIVI_LAUNCHED();
+    for (int hd = 0; hd < qpk; ++hd) {
+        rc = launch_fast<B>(h, qh + hd * U * d, oh + hd * U * d, wh ? wh + hd * U * l : nullptr,
+                            qscale, st);
+        if (rc) return rc;
+    }
+    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(oh, out, U, qpk, d, 0);
+    KIVI_LAUNCHED();
+    if (weights) {
+        if (l % 4 == 0) {
+            permute_heads_kernel<<<grid_for(qpk * U * l / 4), 256, 0, st>>>(wh, weights, U, qpk, l, 0);
+            KIVI_LAUNCHED();
+        } else {
+            for (int hd = 0; hd < qpk; ++hd)
+                KIVI_CUDA(cudaMemcpy2DAsync(weights + hd * l, sizeof(float) * qpk * l,
+                                            wh + hd * U * l, sizeof(float) * l, sizeof(float) * l,
+                                            U, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    h->total_launches += 2 + (weights ? 1 : 0);
+    return KIVI_OK;
+}
+}  // extern "C++"
+
 kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float* out,
                         float* weights, int32_t scale_logits, void* stream) {
     if (!h) return fail(KIVI_ERR_USAGE, "cache is NULL");
@@ -1327,9 +1396,18 @@ kivi_status kivi_attend(kivi_cache* h, const float* t_q, int32_t q_per_kv, float
     DeviceGuard g(h->device);
     cudaStream_t st = S(stream);
     const bool fast_ok = fast_supported(h, q_per_kv) && al16(t_q, out, weights);
-    if (h->attend_path == 2 && !fast_ok)
+    // GQA shapes outside the tensor-core kernel: one MHA fast attend per head
+    const bool heads_ok = !fast_ok && q_per_kv > 1 && fast_supported(h, 1) &&
+                          al16(t_q, out, weights) && tune().gqa_heads;
+    if (h->attend_path == 2 && !fast_ok && !heads_ok)
         return fail(KIVI_ERR_CONFIG,
                     "fast attend path does not support this shape (or rows not 16-byte aligned)");
+    if (heads_ok && h->attend_path != 1) {
+        const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
+        const float qscale = scale * fast::LOG2E;
+        if (h->cfg.bits == 2) return attend_heads_mha<2>(h, t_q, q_per_kv, out, weights, qscale, st);
+        return attend_heads_mha<4>(h, t_q, q_per_kv, out, weights, qscale, st);
+    }
     if (fast_ok && h->attend_path != 1) {
         const float scale = scale_logits ? 1.0f / sqrtf((float)h->cfg.head_dim) : 1.0f;
         const float qscale = scale * fast::LOG2E;

@@ -575,6 +575,21 @@ def test_gqa_fast_vs_reference(cuda, qpk, l0):
     assert ew <= 1e-5, ew
 
 
+@pytest.mark.parametrize("small", ["0", "1"])
+@pytest.mark.parametrize("bits,qpk", [(4, 2), (4, 4), (2, 3), (2, 8), (4, 8)])
+def test_gqa_heads_route(cuda, bits, qpk, small, monkeypatch):
+    """GQA shapes outside the tensor-core kernel (4-bit, or q_per_kv not in
+    {2, 4}) take one MHA fast attend per query head over the shared cache
+    (attend_heads_mha) -- with weights, through the body and few-unit routes,
+    across a key flush -- instead of the generic kernel."""
+    monkeypatch.setenv("KIVI_SMALL_ITEMS", small)
+    l0 = 1150 if small == "0" else 380
+    e, ew = run_gqa((bits, 32, 128, 128), U=3, qpk=qpk, l0=l0, steps=3, path="fast",
+                    seed=bits * 10 + qpk, weights=True)
+    assert e <= 1e-5, e
+    assert ew <= 1e-5, ew
+
+
 # (kscale, vscale, qscale, key outlier channels, tolerance).  The last case
 # has log2-domain logits of magnitude ~500: one fp32 ulp there is 3e-5, so
 # even the reference's own float cast of its double logits (attention.cpp:59-62)
