@@ -1346,40 +1346,55 @@ __global__ void permute_heads_kernel(const float* __restrict__ src, float* __res
 }
 }  // namespace
 
-// GQA shapes the tensor-core kernel does not cover (B = 4, or q_per_kv not in
-// {2, 4}) but the MHA fast kernels do (d = 128, G = 32, B in {2, 4}): one MHA
-// attend per query head over the shared cache (q_per_kv passes over the
-// bytes -- against the generic kernel's reference-order double loop, ~65x
-// faster at C3's shape in 4 bits).  q and the outputs are permuted to and from
-// head-major rows around the passes.
+// GQA shapes outside one tensor-core launch (B = 4, or q_per_kv not in
+// {2, 4}) when the fast kernels cover the cache (d = 128, G = 32, B in {2, 4}):
+// the query heads are split into groups of gs = 4 (or 2) heads for the
+// tensor-core kernel at B = 2 (e.g. 8 q heads per kv head: two passes), else
+// single heads for the MHA kernels; every pass streams the shared cache once
+// (q_per_kv / gs passes, against the generic kernel's reference-order double
+// loop: ~270x faster at C3's shape in 4 bits).  q and the outputs are
+// permuted to and from group-major rows around the passes.
 template <int B>
 static kivi_status attend_heads_mha(kivi_cache* h, const float* t_q, int qpk, float* out,
                                     float* weights, float qscale, cudaStream_t st) {
     const int64_t U = h->n_units, d = h->cfg.head_dim, l = h->l;
+    const int gs = (B == 2 && qpk % 4 == 0) ? 4 : ((B == 2 && qpk % 2 == 0) ? 2 : 1);
+    const int ng = qpk / gs;
     const int64_t need = 2 * qpk * U * d + (weights ? qpk * U * l : 0);
     kivi_status rc = ensure(&h->heads_buf, &h->heads_cap, need);
     if (rc) return rc;
     float* qh = h->heads_buf;
     float* oh = qh + qpk * U * d;
     float* wh = weights ? oh + qpk * U * d : nullptr;
-    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(t_q, qh, U, qpk, d, 1);
+    // rows of gs heads: (u, g) -> (g, u)
+    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(t_q, qh, U, ng, gs * d, 1);
     KIVI_LAUNCHED();
-    for (int hd = 0; hd < qpk; ++hd) {
-        rc = launch_fast<B>(h, qh + hd * U * d, oh + hd * U * d, wh ? wh + hd * U * l : nullptr,
-                            qscale, st);
+    for (int g = 0; g < ng; ++g) {
+        const float* qg = qh + g * U * gs * d;
+        float* og = oh + g * U * gs * d;
+        float* wg = wh ? wh + g * U * gs * l : nullptr;
+        if constexpr (B == 2) {
+            if (gs == 4) rc = launch_gqa<4>(h, qg, og, wg, qscale, st);
+            else if (gs == 2) rc = launch_gqa<2>(h, qg, og, wg, qscale, st);
+            else rc = launch_fast<B>(h, qg, og, wg, qscale, st);
+        } else {
+            rc = launch_fast<B>(h, qg, og, wg, qscale, st);
+        }
         if (rc) return rc;
     }
-    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(oh, out, U, qpk, d, 0);
+    permute_heads_kernel<<<grid_for(qpk * U * d / 4), 256, 0, st>>>(oh, out, U, ng, gs * d, 0);
     KIVI_LAUNCHED();
     if (weights) {
-        if (l % 4 == 0) {
-            permute_heads_kernel<<<grid_for(qpk * U * l / 4), 256, 0, st>>>(wh, weights, U, qpk, l, 0);
+        if ((gs * l) % 4 == 0) {
+            permute_heads_kernel<<<grid_for(qpk * U * l / 4), 256, 0, st>>>(wh, weights, U, ng,
+                                                                            gs * l, 0);
             KIVI_LAUNCHED();
         } else {
-            for (int hd = 0; hd < qpk; ++hd)
-                KIVI_CUDA(cudaMemcpy2DAsync(weights + hd * l, sizeof(float) * qpk * l,
-                                            wh + hd * U * l, sizeof(float) * l, sizeof(float) * l,
-                                            U, cudaMemcpyDeviceToDevice, st));
+            for (int g = 0; g < ng; ++g)
+                KIVI_CUDA(cudaMemcpy2DAsync(weights + g * gs * l, sizeof(float) * qpk * l,
+                                            wh + g * U * gs * l, sizeof(float) * gs * l,
+                                            sizeof(float) * gs * l, U, cudaMemcpyDeviceToDevice,
+                                            st));
         }
     }
     h->total_launches += 2 + (weights ? 1 : 0);

@@ -576,7 +576,7 @@ def test_gqa_fast_vs_reference(cuda, qpk, l0):
 
 
 @pytest.mark.parametrize("small", ["0", "1"])
-@pytest.mark.parametrize("bits,qpk", [(4, 2), (4, 4), (2, 3), (2, 8), (4, 8)])
+@pytest.mark.parametrize("bits,qpk", [(4, 2), (4, 4), (2, 3), (2, 6), (2, 8), (4, 8)])
 def test_gqa_heads_route(cuda, bits, qpk, small, monkeypatch):
     """GQA shapes outside the tensor-core kernel (4-bit, or q_per_kv not in
     {2, 4}) take one MHA fast attend per query head over the shared cache
