@@ -31,6 +31,12 @@ struct AttendGenericArgs {
 // exp rounded from a double evaluation (closest float to e^x in practice).
 __device__ __forceinline__ float expf_accurate(float x) { return (float)exp((double)x); }
 
+// Group scales (the reference's double (hi - lo) / maxc) are computed once per
+// group into shared memory, a batch of key tiles / value tokens at a time,
+// instead of once per code (a DDIV per element): the same doubles, the same
+// summation order, so the outputs are unchanged bit for bit.
+constexpr int GEN_SC_CAP = 1024;  // cached (scale, zero) entries: 12 KB
+
 __global__ void attend_generic_kernel(AttendGenericArgs a) {
     extern __shared__ float smem[];
     const CacheDev& c = a.c;
@@ -40,6 +46,8 @@ __global__ void attend_generic_kernel(AttendGenericArgs a) {
     const int64_t row = u * a.qpk + h;
     float* sq = smem;             // d
     float* red = smem + d;        // 32 floats
+    double* sS = reinterpret_cast<double*>(smem + ((d + 32 + 1) & ~1));  // GEN_SC_CAP
+    float* sZ = reinterpret_cast<float*>(sS + GEN_SC_CAP);                // GEN_SC_CAP
     const float* q = a.q + row * d;
     for (int ch = threadIdx.x; ch < d; ch += blockDim.x) sq[ch] = q[ch];
     __syncthreads();
@@ -54,28 +62,52 @@ __global__ void attend_generic_kernel(AttendGenericArgs a) {
     const float* kr = c.kring + u * c.ring_ustride;
     const float* vr = c.vring + u * c.ring_ustride;
 
-    // 1. logits
-    for (int64_t t = threadIdx.x; t < l; t += blockDim.x) {
-        float logit;
-        if (t < kg) {
-            const int64_t tg = t / G, i = t % G;
-            double acc = 0.0;
-            for (int ch = 0; ch < d; ++ch) {
-                const int64_t g = tg * d + ch;
-                const float2 pr = kp[g];
-                const double s = group_scale(pr.x, pr.y, c.maxc);
-                const uint32_t code = read_code(kc, ((uint64_t)g * G + i) * c.bits, c.bits);
-                const double deq = __dadd_rn(__dmul_rn((double)code, s), (double)pr.x);
-                acc = __dadd_rn(acc, __dmul_rn((double)sq[ch], deq));
+    // 1. logits of the grouped keys: nt tiles at a time (their d x nt scales
+    //    cached), one thread per token, channels in order
+    {
+        const int T = max(1, min((int)blockDim.x / G, GEN_SC_CAP / d));
+        const int64_t ntiles = kg / G;
+        for (int64_t tg0 = 0; tg0 < ntiles; tg0 += T) {
+            const int nt = (int)(ntiles - tg0 < T ? ntiles - tg0 : T);
+            if (d <= GEN_SC_CAP) {
+                for (int e = threadIdx.x; e < nt * d; e += blockDim.x) {
+                    const float2 pr = kp[(tg0 + e / d) * d + e % d];
+                    sS[e] = group_scale(pr.x, pr.y, c.maxc);
+                    sZ[e] = pr.x;
+                }
             }
-            logit = (float)acc;
-        } else {
-            const float* kv = kr + (t - kg) * d;
-            float acc = 0.0f;
-            for (int ch = 0; ch < d; ++ch) acc = __fadd_rn(acc, __fmul_rn(sq[ch], kv[ch]));
-            logit = acc;
+            __syncthreads();
+            for (int j = threadIdx.x; j < nt * G; j += blockDim.x) {
+                const int tt = j / G, i = j % G;
+                const int64_t tg = tg0 + tt, t = tg * G + i;
+                double acc = 0.0;
+                for (int ch = 0; ch < d; ++ch) {
+                    const int64_t g = tg * d + ch;
+                    double s;
+                    float z;
+                    if (d <= GEN_SC_CAP) {
+                        s = sS[tt * d + ch];
+                        z = sZ[tt * d + ch];
+                    } else {
+                        const float2 pr = kp[g];
+                        s = group_scale(pr.x, pr.y, c.maxc);
+                        z = pr.x;
+                    }
+                    const uint32_t code = read_code(kc, ((uint64_t)g * G + i) * c.bits, c.bits);
+                    const double deq = __dadd_rn(__dmul_rn((double)code, s), (double)z);
+                    acc = __dadd_rn(acc, __dmul_rn((double)sq[ch], deq));
+                }
+                lg[t] = __fmul_rn((float)acc, scale);
+            }
+            __syncthreads();
         }
-        lg[t] = __fmul_rn(logit, scale);
+    }
+    // residual keys
+    for (int64_t t = kg + threadIdx.x; t < l; t += blockDim.x) {
+        const float* kv = kr + (t - kg) * d;
+        float acc = 0.0f;
+        for (int ch = 0; ch < d; ++ch) acc = __fadd_rn(acc, __fmul_rn(sq[ch], kv[ch]));
+        lg[t] = __fmul_rn(acc, scale);
     }
     __syncthreads();
 
@@ -111,8 +143,53 @@ __global__ void attend_generic_kernel(AttendGenericArgs a) {
     }
     __syncthreads();
 
-    // 4. outputs
+    // 4. outputs: grouped values in token chunks (their scales cached), one
+    //    thread per channel (up to 8 channels per thread), tokens in order
     const int gpt = d / G;
+    constexpr int CPT = 8;
+    if (d <= CPT * (int)blockDim.x && gpt <= GEN_SC_CAP) {
+        double acc[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) acc[k] = 0.0;
+        const int TC = max(1, GEN_SC_CAP / gpt);
+        for (int64_t t0 = 0; t0 < vg; t0 += TC) {
+            const int nt = (int)(vg - t0 < TC ? vg - t0 : TC);
+            for (int e = threadIdx.x; e < nt * gpt; e += blockDim.x) {
+                const float2 pr = vp[t0 * gpt + e];
+                sS[e] = group_scale(pr.x, pr.y, c.maxc);
+                sZ[e] = pr.x;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int ch = threadIdx.x + k * blockDim.x;
+                if (ch < d) {
+                    double ac = acc[k];
+                    for (int tt = 0; tt < nt; ++tt) {
+                        const int64_t t = t0 + tt;
+                        const double w = (double)lg[t];
+                        const int e = tt * gpt + ch / G;
+                        const uint32_t code = read_code(vc, ((uint64_t)t * d + ch) * c.bits, c.bits);
+                        ac = __dadd_rn(ac, __dmul_rn(w, __dadd_rn(__dmul_rn((double)code, sS[e]),
+                                                                  (double)sZ[e])));
+                    }
+                    acc[k] = ac;
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int ch = threadIdx.x + k * blockDim.x;
+            if (ch < d) {
+                float r = 0.0f;
+                for (int64_t t = vg; t < l; ++t)
+                    r = __fadd_rn(r, __fmul_rn(lg[t], vr[(t % a.ring_mod) * d + ch]));
+                a.out[row * d + ch] = vg > 0 ? __fadd_rn(r, (float)acc[k]) : r;
+            }
+        }
+        return;
+    }
     for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
         double acc = 0.0;
         for (int64_t t = 0; t < vg; ++t) {

@@ -973,6 +973,12 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     return KIVI_OK;
 }
 
+// attend_generic_kernel's dynamic shared memory: q row, reduction scratch,
+// and the cached group (scale, zero) pairs
+size_t generic_smem(int64_t d) {
+    return sizeof(float) * (size_t)((d + 32 + 1) & ~1LL) + (sizeof(double) + sizeof(float)) * GEN_SC_CAP;
+}
+
 kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, float* weights,
                            int scale_logits, cudaStream_t st) {
     const int64_t rows = h->n_units * qpk;
@@ -990,7 +996,7 @@ kivi_status launch_generic(kivi_cache* h, const float* q, int qpk, float* out, f
     a.weights = weights;
     a.scratch = h->scratch;
     a.scale_logits = scale_logits;
-    const size_t smem = sizeof(float) * (size_t)(h->cfg.head_dim + 32);
+    const size_t smem = generic_smem(h->cfg.head_dim);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
     if (h->prof_now) {
@@ -2414,7 +2420,7 @@ kivi_status kivi_reference_attention(const float* q, int64_t n_q, const float* k
     a.weights = nullptr;
     a.scratch = lg_scratch;
     a.scale_logits = scale_logits;
-    attend_generic_kernel<<<(unsigned)n_q, 256, sizeof(float) * (size_t)(d + 32), st>>>(a);
+    attend_generic_kernel<<<(unsigned)n_q, 256, generic_smem(d), st>>>(a);
     cudaError_t le = cudaGetLastError();
     cudaError_t se = cudaStreamSynchronize(st);
     if (le != cudaSuccess) return fail(KIVI_ERR_CUDA, "reference_attention: %s", cudaGetErrorString(le));
