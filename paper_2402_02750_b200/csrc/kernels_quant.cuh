@@ -374,6 +374,32 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
     append_unit_fast<B, false>(c, tk, tv, l, u, lane);
 }
 
+// Flush warp fw of an early key-tile quantisation: (unit, tile tl0 + ..,
+// 32-channel slice) = one group per lane (see append_flush_fast_kernel).
+template <int B>
+__device__ __forceinline__ void flush_key_group(const CacheDev& c, const float* __restrict__ tk,
+                                                int64_t l, int64_t fw, int tl0, int ntl, int lane) {
+    constexpr int D = 128, G = 32;
+    const int64_t u = fw / (ntl * (D / 32));
+    if (u >= c.n_units) return;
+    const int rem = (int)(fw % (ntl * (D / 32)));
+    const int tl = tl0 + rem / (D / 32);
+    const int ch = (rem % (D / 32)) * 32 + lane;
+    const float* kring = c.kring + u * c.ring_ustride;
+    const int last = (int)(l % c.R);  // ring row of token l (written by this launch)
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int r = tl * G + i;
+        x[i] = (r == last && tk) ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
+    }
+    uint32_t w[B];
+    const float2 lh = key_group_fast<B>(x, w);
+    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
+    store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
+    c.kpairs[u * c.kp_ustride + g] = lh;
+}
+
 // Append plus early key-tile quantisation: blocks [0, n_app) append one unit
 // per warp (no flush); the remaining blocks quantize ring tiles
 // [tl0, tl0 + ntl) of the current window (kg = l - l % R), one thread per
@@ -407,24 +433,7 @@ __global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
         return;
     }
     const int64_t fw = (int64_t)(blockIdx.x - n_app) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t u = fw / (ntl * (D / 32));
-    if (u >= c.n_units) return;
-    const int rem = (int)(fw % (ntl * (D / 32)));
-    const int tl = tl0 + rem / (D / 32);
-    const int ch = (rem % (D / 32)) * 32 + lane;
-    const float* kring = c.kring + u * c.ring_ustride;
-    const int last = (int)(l % c.R);  // ring row of token l (written by this launch)
-    float x[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const int r = tl * G + i;
-        x[i] = (r == last && tk) ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
-    }
-    uint32_t w[B];
-    const float2 lh = key_group_fast<B>(x, w);
-    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
-    store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
-    c.kpairs[u * c.kp_ustride + g] = lh;
+    flush_key_group<B>(c, tk, l, fw, tl0, ntl, lane);
 }
 
 // ---- bulk prefill for d = 128, G = 32, B in {2, 4} --------------------------

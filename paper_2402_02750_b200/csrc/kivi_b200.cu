@@ -124,6 +124,9 @@ struct kivi_cache {
     int64_t scratch_cap = 0;
     float* heads_buf = nullptr;  // per-head GQA route: q / out (/ weights) by head
     int64_t heads_cap = 0;
+    // launch_fast(defer_combine): the merge left to the caller
+    int64_t pending_nsub = 0;
+    int pending_cmode = 0;
     float2* stats = nullptr;
     int64_t stats_cap = 0;
     // [B][body, tail, gqa_tc, small_fused, body_vimma, body 512, body_vimma 512]
@@ -337,7 +340,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
-    int body_prefetch, body_long_l, gqa_heads;
+    int body_prefetch, body_long_l, gqa_heads, step_fuse;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -360,6 +363,7 @@ struct Tuning {
         body_prefetch = env_int("KIVI_BODY_PREFETCH", 0);
         body_long_l = env_int("KIVI_BODY_LONG_L", 16384);
         gqa_heads = env_int("KIVI_GQA_HEADS", 1);
+        step_fuse = env_int("KIVI_STEP_FUSE", 1);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -552,7 +556,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st, const float* tk = nullptr, const float* tv = nullptr,
-                        int64_t l_app = -1) {
+                        int64_t l_app = -1, bool defer_combine = false) {
     const int64_t U = h->n_units;
     // Items: body = whole BSUB-token sub-chunks below floor32(vg) (all keys and
     // values quantized); tail = TSUB-token items over [nfull * BSUB, l), which
@@ -823,6 +827,11 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     // balanced; fusing it into the attend tail serialised it on the last warps)
     const int cmode = combine_parallel(U);
     const unsigned cgrid = (unsigned)(cmode == 2 ? ceil_div(U, 4) : U);
+    if (defer_combine) {  // the caller fuses the merge with the next layer's append
+        h->pending_nsub = n_sub;
+        h->pending_cmode = cmode;
+        return KIVI_OK;
+    }
     if (use_pdl && ((nfull == 0 && !h->prof_now) || (one_stream && !h->prof_now)))
         KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3(cgrid), dim3(fast::D), 0, st,
                              (const float*)h->part_o, (const float2*)h->part_ml, (int)n_sub, out,
@@ -1642,12 +1651,88 @@ static kivi_status check_layers(kivi_cache* const* caches, int32_t n_layers) {
     return KIVI_OK;
 }
 
+// Whether a multi-layer step can fuse each layer's merge with the next layer's
+// append (combine_append_kernel): MHA on the fast kernels' body route, no
+// profiling, every layer at the same length and shape.
+static bool step_fusable(kivi_cache* const* caches, int32_t n_layers, int32_t q_per_kv,
+                         const float* t_q, const float* t_k, const float* t_v, const float* out) {
+    if (!tune().step_fuse || n_layers < 2 || q_per_kv != 1 || !tune().pdl) return false;
+    if (!al16(t_q, t_k, t_v, out)) return false;
+    const kivi_cache* h0 = caches[0];
+    for (int32_t i = 0; i < n_layers; ++i) {
+        const kivi_cache* h = caches[i];
+        if (!fast_supported(h, 1) || h->attend_path == 1 || h->profile || h->l != h0->l ||
+            h->cfg.bits != h0->cfg.bits || h->cfg.residual_length != h0->cfg.residual_length ||
+            h->kq_done != h0->kq_done || small_fused_ok(h, 1) || fused_append_ok(h, 1))
+            return false;
+        // body route after this step's append (the few-unit route has its own chain)
+        const int64_t l = h->l + 1;
+        if (tune().small_items && h->n_units * ceil_div(l, fast::BSUB) < 4 * num_sms()) return false;
+        const int64_t vg = l - std::min<int64_t>(l, h->cfg.residual_length);
+        if ((vg / 32 * 32) / fast::BSUB == 0) return false;
+    }
+    return true;
+}
+
+extern "C++" {
+template <int B>
+static kivi_status decode_layers_fused(kivi_cache* const* caches, int32_t n_layers,
+                                       const float* t_q, const float* t_k, const float* t_v,
+                                       float* out, int32_t scale_logits, cudaStream_t st) {
+    const int64_t U = caches[0]->n_units, d = caches[0]->cfg.head_dim;
+    const int64_t krow = U * d;
+    const float qscale = (scale_logits ? 1.0f / sqrtf((float)d) : 1.0f) * fast::LOG2E;
+    for (int32_t i = 0; i < n_layers; ++i) {
+        kivi_status rc = ensure_capacity(caches[i], caches[i]->l + 1, st);
+        if (rc) return rc;
+    }
+    kivi_status rc = append_launch(caches[0], t_k, t_v, st);
+    if (rc) return rc;
+    append_bookkeeping(caches[0]);
+    for (int32_t i = 0; i < n_layers; ++i) {
+        kivi_cache* h = caches[i];
+        rc = launch_fast<B>(h, t_q + i * krow, out + i * krow, nullptr, qscale, st, nullptr,
+                            nullptr, -1, /*defer_combine=*/true);
+        if (rc) return rc;
+        const int n_sub = (int)h->pending_nsub, cmode = h->pending_cmode;
+        const int n_comb = (int)(cmode == 2 ? ceil_div(U, 4) : U);
+        if (i + 1 < n_layers) {
+            kivi_cache* hn = caches[i + 1];
+            int tl0, ntl;
+            key_tiles_due(hn, &tl0, &ntl);
+            const int n_app = (int)ceil_div(U, 4);
+            const int n_fl = ntl > 0 ? (int)ceil_div(U * ntl * 128, 128) : 0;
+            KIVI_CUDA(launch_pdl(fast::combine_append_kernel<B>, dim3((unsigned)(n_comb + n_app + n_fl)),
+                                 dim3(fast::D), 0, st, (const float*)h->part_o,
+                                 (const float2*)h->part_ml, n_sub, out + i * krow, cmode, (int64_t)U,
+                                 n_comb, hn->dev, t_k + (i + 1) * krow, t_v + (i + 1) * krow,
+                                 (int64_t)hn->l, n_app, tl0, ntl));
+            KIVI_LAUNCHED();
+            h->total_launches++;
+            append_bookkeeping(hn);
+        } else {
+            KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)n_comb), dim3(fast::D), 0, st,
+                                 (const float*)h->part_o, (const float2*)h->part_ml, n_sub,
+                                 out + i * krow, (float2*)nullptr, cmode, (int64_t)U));
+            KIVI_LAUNCHED();
+            h->total_launches++;
+        }
+    }
+    return KIVI_OK;
+}
+}  // extern "C++"
+
 static kivi_status decode_layers_enqueue(kivi_cache* const* caches, int32_t n_layers,
                                          const float* t_q, const float* t_k, const float* t_v,
                                          int32_t q_per_kv, float* out, int32_t scale_logits,
                                          void* stream) {
     const int64_t U = caches[0]->n_units, d = caches[0]->cfg.head_dim;
     const int64_t qrow = U * q_per_kv * d, krow = U * d;
+    if (step_fusable(caches, n_layers, q_per_kv, t_q, t_k, t_v, out)) {
+        if (caches[0]->cfg.bits == 2)
+            return decode_layers_fused<2>(caches, n_layers, t_q, t_k, t_v, out, scale_logits, S(stream));
+        return decode_layers_fused<4>(caches, n_layers, t_q, t_k, t_v, out, scale_logits, S(stream));
+    }
     for (int32_t i = 0; i < n_layers; ++i) {
         kivi_status rc = kivi_decode(caches[i], t_q + i * qrow, t_k + i * krow, t_v + i * krow,
                                      q_per_kv, out + i * qrow, nullptr, scale_logits, stream);

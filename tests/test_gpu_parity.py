@@ -846,7 +846,7 @@ def test_export_cache_unit_kvqd(cuda, tmp_path):
 
 
 @pytest.mark.parametrize("graph", ["0", "1"])
-@pytest.mark.parametrize("qpk,U,l0", [(1, 3, 700), (1, 64, 2300), (4, 4, 900)])
+@pytest.mark.parametrize("qpk,U,l0", [(1, 3, 700), (1, 64, 2300), (1, 80, 2300), (4, 4, 900)])
 def test_decode_layers_equals_per_layer(cuda, graph, qpk, U, l0, monkeypatch):
     """kivi_decode_layers / kivi_decode_layers_host (one call per model step,
     optionally replayed as a CUDA graph) give bit-identical outputs and states
