@@ -129,8 +129,9 @@ struct kivi_cache {
     int pending_cmode = 0;
     float2* stats = nullptr;
     int64_t stats_cap = 0;
-    // [B][body, tail, gqa_tc, small_fused, body_vimma, body 512, body_vimma 512]
-    int fast_per_sm[9][7] = {};
+    // [B][body, tail, gqa_tc, small_fused, body_vimma, body 512, body_vimma 512,
+    //     body 384, body_vimma 384]
+    int fast_per_sm[9][9] = {};
     // staging for _host calls
     // host-path staging, double-buffered: call i uploads into stg[i & 1]
     // while call i-1's kernels may still read stg[(i-1) & 1]
@@ -340,7 +341,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
-    int body_prefetch, body_long_l, gqa_heads, step_fuse;
+    int body_prefetch, body_long_l, gqa_heads, step_fuse, body_sub;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -364,6 +365,7 @@ struct Tuning {
         body_long_l = env_int("KIVI_BODY_LONG_L", 16384);
         gqa_heads = env_int("KIVI_GQA_HEADS", 1);
         step_fuse = env_int("KIVI_STEP_FUSE", 1);
+        body_sub = env_int("KIVI_BODY_SUB", -1);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -553,6 +555,31 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Tokens per body item.  KIVI_BODY_SUB = 256 / 384 / 512 fixes it; -1 (auto):
+// the largest item size whose whole items cover [0, floor32(vg)) within 2 %
+// of the best size (what they leave goes to the residual-window kernel);
+// larger items = fewer items, less per-item work.  C2 / C4 (vg ~ 3968) ->
+// 384 (attend -1.9 %), C5 (vg = 32640) -> 512 (-2.4 %).  -2: the earlier
+// rule, 512 from KIVI_BODY_LONG_L tokens, else 256.
+static int body_item_tokens(const kivi_cache* h, int64_t body_vg, int64_t l_app) {
+    if (l_app >= 0 || tune().mha_tc) return fast::BSUB;
+    const int fixed = tune().body_sub;
+    if (fixed == 256 || fixed == 384 || fixed == 512) return fixed;
+    if (fixed == -2) {
+        const int long_l = tune().body_long_l;
+        return (long_l > 0 && h->l >= long_l) ? 512 : fast::BSUB;
+    }
+    const int64_t span = (body_vg / 32) * 32;
+    int64_t best_cover = 0;
+    for (int bs : {256, 384, 512}) best_cover = std::max(best_cover, (span / bs) * bs);
+    // the largest item whose whole items cover within 2 % of the best
+    for (int bs : {512, 384}) {
+        const int64_t cover = (span / bs) * bs;
+        if (cover > 0 && 50 * (best_cover - cover) <= span) return bs;
+    }
+    return fast::BSUB;
+}
+
 template <int B>
 kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weights, float qscale,
                         cudaStream_t st, const float* tk = nullptr, const float* tv = nullptr,
@@ -586,8 +613,7 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int64_t body_vg = l_app >= 0 ? h->vg() - 1 : h->vg();
     // body item size: 512 tokens from KIVI_BODY_LONG_L tokens (default 16384;
     // 0 disables), where the wider residual region is a small share
-    const int long_l = tune().body_long_l;
-    const int bsub = (long_l > 0 && h->l >= long_l && l_app < 0 && !tune().mha_tc) ? 512 : fast::BSUB;
+    const int bsub = body_item_tokens(h, body_vg, l_app);
     const int64_t nfull = latency_bound ? 0 : ((body_vg / 32) * 32) / bsub;
     if (l_app >= 0 && (latency_bound || nfull == 0))
         return fail(KIVI_ERR_USAGE, "internal: fused append outside its route");
@@ -633,16 +659,20 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
     const int smem = fast::WS2::STRIDE * fast::WARPS;
     // P.V of the body on the integer tensor cores (2-bit; kernels_vimma.cuh)
     const bool vimma = B == 2 && tune().vimma;
-    const bool b512 = bsub == 512;
+    const int bidx = bsub == 512 ? 1 : (bsub == 384 ? 2 : 0);
     const int smem_body =
-        (b512 ? (vimma ? fast::WarpSmemBody<true, 512>::STRIDE : fast::WarpSmemBody<false, 512>::STRIDE)
-              : (vimma ? fast::WarpSmemBody<true>::STRIDE : fast::WSB::STRIDE)) *
+        (bidx == 1 ? (vimma ? fast::WarpSmemBody<true, 512>::STRIDE : fast::WarpSmemBody<false, 512>::STRIDE)
+         : bidx == 2 ? (vimma ? fast::WarpSmemBody<true, 384>::STRIDE : fast::WarpSmemBody<false, 384>::STRIDE)
+                     : (vimma ? fast::WarpSmemBody<true>::STRIDE : fast::WSB::STRIDE)) *
         fast::WARPS;
     void (*body_kernel)(fast::FastArgs) =
-        b512 ? fast::attend_body_kernel<B, false, 512> : fast::attend_body_kernel<B>;
+        bidx == 1 ? fast::attend_body_kernel<B, false, 512>
+                  : (bidx == 2 ? fast::attend_body_kernel<B, false, 384> : fast::attend_body_kernel<B>);
     if constexpr (B == 2)
         if (vimma)
-            body_kernel = b512 ? fast::attend_body_kernel<2, true, 512> : fast::attend_body_kernel<2, true>;
+            body_kernel = bidx == 1 ? fast::attend_body_kernel<2, true, 512>
+                                    : (bidx == 2 ? fast::attend_body_kernel<2, true, 384>
+                                                 : fast::attend_body_kernel<2, true>);
     const int smem_tc = gqa_tc::TS<1>::STRIDE * gqa_tc::WARPS;
     const int mha_tc = tune().mha_tc;  // measured slower on C2
     if (h->fast_per_sm[B][0] == 0) {
@@ -679,6 +709,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &per_sm, fast::attend_body_kernel<2, true, 512>, fast::WARPS * 32, smem_vi5));
             h->fast_per_sm[B][6] = per_sm < 1 ? 1 : per_sm;
+            const int smem_vi3 = fast::WarpSmemBody<true, 384>::STRIDE * fast::WARPS;
+            KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<2, true, 384>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_vi3));
+            KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, fast::attend_body_kernel<2, true, 384>, fast::WARPS * 32, smem_vi3));
+            h->fast_per_sm[B][8] = per_sm < 1 ? 1 : per_sm;
         }
         {
             const int smem5 = fast::WarpSmemBody<false, 512>::STRIDE * fast::WARPS;
@@ -687,6 +723,12 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
             KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &per_sm, fast::attend_body_kernel<B, false, 512>, fast::WARPS * 32, smem5));
             h->fast_per_sm[B][5] = per_sm < 1 ? 1 : per_sm;
+            const int smem3 = fast::WarpSmemBody<false, 384>::STRIDE * fast::WARPS;
+            KIVI_CUDA(cudaFuncSetAttribute(fast::attend_body_kernel<B, false, 384>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
+            KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, fast::attend_body_kernel<B, false, 384>, fast::WARPS * 32, smem3));
+            h->fast_per_sm[B][7] = per_sm < 1 ? 1 : per_sm;
         }
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, fast::attend_tail_kernel<B>, fast::WARPS * 32, smem));
@@ -793,7 +835,8 @@ kivi_status launch_fast(kivi_cache* h, const float* q, float* out, float* weight
                 <<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
         } else {
             const int64_t grid = std::min<int64_t>(
-                (int64_t)num_sms() * h->fast_per_sm[B][b512 ? (vimma ? 6 : 5) : (vimma ? 4 : 0)],
+                (int64_t)num_sms() *
+                    h->fast_per_sm[B][bidx == 1 ? (vimma ? 6 : 5) : bidx == 2 ? (vimma ? 8 : 7) : (vimma ? 4 : 0)],
                 ceil_div(a.n_items, fast::WARPS));
             if (tail_deferred) {
                 // body first (normal launch: the append is complete), then the

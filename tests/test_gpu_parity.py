@@ -381,13 +381,15 @@ def test_decode_fast_vs_reference(cuda, bits, l0, route, monkeypatch):
     assert e_w <= 1e-5, e_w
 
 
+@pytest.mark.parametrize("sub", ["384", "512", "-1"])
 @pytest.mark.parametrize("vimma", ["1", "0"])
 @pytest.mark.parametrize("bits", [2, 4])
 @pytest.mark.parametrize("l0", [1100, 1535, 2049])
-def test_body_512_token_items(cuda, bits, l0, vimma, monkeypatch):
-    """The body kernel's 512-token items (chosen from KIVI_BODY_LONG_L tokens,
-    16384 by default; lowered here so short contexts take them), with weights."""
-    monkeypatch.setenv("KIVI_BODY_LONG_L", "1000")
+def test_body_item_sizes(cuda, bits, l0, vimma, sub, monkeypatch):
+    """The body kernel's 384- and 512-token items (KIVI_BODY_SUB fixes the
+    size; -1, the default, takes the size covering the most tokens), with
+    weights."""
+    monkeypatch.setenv("KIVI_BODY_SUB", sub)
     monkeypatch.setenv("KIVI_SMALL_ITEMS", "0")
     monkeypatch.setenv("KIVI_VIMMA", vimma)
     e_out, e_w = run_decode((bits, 32, 128, 128), U=3, l0=l0, steps=4, path="fast",
