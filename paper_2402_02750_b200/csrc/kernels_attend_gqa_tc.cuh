@@ -104,7 +104,10 @@ __device__ __forceinline__ int pblock(int p) {
     return H == 4 ? p ^ ((p >> 2) & 3) : p;
 }
 
-template <int H>
+// IT: tokens per item.  IT = 384 keeps the per-warp footprint inside 3 CTAs x
+// 4 warps per SM by single-buffering the B fragments (one more warp barrier
+// per tile / K step).
+template <int H, int IT = SUB>
 struct TS {  // per-warp shared memory
     // q rows are staged (TMA) into the key-bias scratch: q is consumed at the
     // start of an item, the scratch only afterwards, and the next item's q
@@ -112,14 +115,15 @@ struct TS {  // per-warp shared memory
     static constexpr int QB_OFF = 2 * SLOT;                   // [H][128] q | [32][17] bias
     static constexpr int QB_BYTES = (32 * BIAS_ROW * 4 > H * D * 4) ? 32 * BIAS_ROW * 4 : H * D * 4;
     static constexpr int PROBS_OFF = QB_OFF + ((QB_BYTES + 15) & ~15);  // [256 x H] p (pidx)
-    static constexpr int BF_OFF = PROBS_OFF + SUB * H * 4;     // B fragments (keys | values)
+    static constexpr int BF_OFF = PROBS_OFF + IT * H * 4;      // B fragments (keys | values)
     static constexpr int BFK_BYTES = 32 * BFK_ROW * 8;         // 2304 = 2 x 4 x 72 x 4
-    static constexpr int BF_BYTES = 2 * BFK_BYTES;            // double-buffered
+    static constexpr bool DB = IT <= SUB;                     // double-buffered fragments
+    static constexpr int BF_BYTES = (DB ? 2 : 1) * BFK_BYTES;
     static constexpr int ZS_OFF = BF_OFF + BF_BYTES;           // [H][4] value z sums
     static constexpr int BAR_OFF = ZS_OFF + 16 * 4;
     static constexpr int BYTES = BAR_OFF + 16;
     static constexpr int STRIDE = (BYTES + 127) & ~127;
-    static_assert(2 * 4 * BFV_CG * 4 <= BF_BYTES, "value B buffers overflow");
+    static_assert((DB ? 2 : 1) * 4 * BFV_CG * 4 <= BF_BYTES, "value B buffers overflow");
     static_assert(BFK_BYTES % 16 == 0, "key B buffer alignment");
 };
 
@@ -196,7 +200,7 @@ __device__ __forceinline__ void mma_f16_x2(float4& d0, float4& d1, const CodeQua
 // One key job: KT tiles (codes [KT][1024 B], pairs [KT][128] (lo, hi)) -> the
 // log2-domain logits of tokens tok0 .. tok0+32KT-1 x H heads at probs[pidx].
 // -------------------------------------------------------------------------
-template <int H>
+template <int H, bool DB = true>
 __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[H][2], float qmax,
                                         float* probs, int tok0, uint8_t* bf, float* biasm, int lane,
                                         uint32_t sel, int ntl) {
@@ -245,7 +249,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     const int s_p = lane >> 2, t_p = lane & 3;  // producer -> consumer K step / lane slot
     // producer: B fragments of tile T into buffer T & 1
     auto produce = [&](int T) {
-        uint2* bfk = reinterpret_cast<uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
+        uint2* bfk = reinterpret_cast<uint2*>(bf + (DB ? (T & 1) : 0) * TS<H>::BFK_BYTES);
         const float4 p01 = pairs4[T * 64 + lane];
         const float4 p23 = pairs4[T * 64 + 32 + lane];
         const float2 f2 = make_float2(f, f);
@@ -262,7 +266,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
     };
     // consumer: 8 K steps x 2 MMAs of tile T, then its logits
     auto consume = [&](int T) {
-        const uint2* bfk = reinterpret_cast<const uint2*>(bf + (T & 1) * TS<H>::BFK_BYTES);
+        const uint2* bfk = reinterpret_cast<const uint2*>(bf + (DB ? (T & 1) : 0) * TS<H>::BFK_BYTES);
         // even / odd K steps accumulate separately: two independent HMMA
         // chains per token half
         float4 acc[2][2];
@@ -312,6 +316,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
             produce(T);
             __syncwarp();
             consume(T);
+            if (!DB) __syncwarp();  // one buffer: the next producer overwrites it
         }
     }
 #else
@@ -320,6 +325,7 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
         produce(T);
         __syncwarp();
         consume(T);
+        if (!DB) __syncwarp();
     }
 #endif
     __syncwarp();  // the next job's producer overwrites the buffers
@@ -328,13 +334,14 @@ __device__ __forceinline__ void key_job(const uint8_t* slot, const float2 (&qv)[
 // Softmax of each head over the item's 256 tokens (probs in pidx layout, in
 // place, log2 domain) -> p in (0, 1]; ml[h] = (max, sum).  Lane L owns the
 // pair blocks L + 32i (tokens tb, tb+4 with tb = (b >> 2) * 8 + (b & 3)).
-template <int H>
+template <int H, int IT = SUB>
 __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t wstride, float2* ml,
-                                              int lane, int ntok = SUB) {
+                                              int lane, int ntok = IT) {
+    constexpr int NP = IT / 64;  // pair blocks per lane
     __syncwarp();
-    float2 v[4][H];
+    float2 v[NP][H];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NP; ++i) {
         if constexpr (H == 1) {
             v[i][0] = reinterpret_cast<const float2*>(probs)[lane + 32 * i];
         } else {
@@ -352,13 +359,13 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
     for (int h = 0; h < H; ++h) {
         m[h] = fmaxf(v[0][h].x, v[0][h].y);
 #pragma unroll
-        for (int i = 1; i < 4; ++i) m[h] = fmaxf(m[h], fmaxf(v[i][h].x, v[i][h].y));
+        for (int i = 1; i < NP; ++i) m[h] = fmaxf(m[h], fmaxf(v[i][h].x, v[i][h].y));
         m[h] = warp_max_redux(m[h]);
         sm[h] = 0.f;
     }
     if (wlog) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < NP; ++i) {
             const int b = pblock<H>(lane + 32 * i);
             const int tb = (b >> 2) * 8 + (b & 3);
 #pragma unroll
@@ -369,7 +376,7 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NP; ++i) {
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             v[i][h].x = fast::ex2_approx(v[i][h].x - m[h]);
@@ -397,7 +404,7 @@ __device__ __forceinline__ void softmax_heads(float* probs, float* wlog, int64_t
 // (this lane's share of sum_t p_h[t] z[t][cg = lane & 3], token pair halves).  eb_run is the running
 // exponent byte (the larger of all jobs so far: smaller 2^E).
 // -------------------------------------------------------------------------
-template <int H, bool FULL = true>
+template <int H, bool FULL = true, bool DB = true>
 __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_src, float4 (&vacc)[4][2],
                                           float2 (&zs)[H], int& eb_run, bool first, uint8_t* bf,
                                           int lane, uint32_t sel, int ntok = VT) {
@@ -433,7 +440,7 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
     const int toff = (p < 4) ? p : p + 4;  // this producer's token pair: (toff, toff + 4)
     // producer: B fragments of K step s into buffer s & 1
     auto produce = [&](int s) {
-        uint32_t* bv = reinterpret_cast<uint32_t*>(bf) + (s & 1) * (4 * BFV_CG);
+        uint32_t* bv = reinterpret_cast<uint32_t*>(bf) + (DB ? (s & 1) : 0) * (4 * BFV_CG);
         const int ta = 16 * s + toff, tb = ta + 4;
         // tokens past a partial item's end: zero operands (their slot bytes
         // were not loaded)
@@ -467,7 +474,7 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
     };
     // consumer: 4 channel groups x 2 MMAs of K step s
     auto consume = [&](int s) {
-        const uint32_t* bv = reinterpret_cast<const uint32_t*>(bf) + (s & 1) * (4 * BFV_CG);
+        const uint32_t* bv = reinterpret_cast<const uint32_t*>(bf) + (DB ? (s & 1) : 0) * (4 * BFV_CG);
 #pragma unroll
         for (int cg = 0; cg < 4; ++cg) {
             const uint8_t* cw = slot + 4 * (2 * cg + (g >> 2)) + (16 * s + t) * 32;
@@ -490,6 +497,7 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
             produce(s);
             __syncwarp();
             consume(s);
+            if (!DB) __syncwarp();  // one buffer: the next producer overwrites it
         }
     } else
 #endif
@@ -499,6 +507,7 @@ __device__ __forceinline__ void value_job(const uint8_t* slot, const float* p_sr
             produce(s);
             __syncwarp();
             consume(s);
+            if (!DB) __syncwarp();
         }
     }
 }
@@ -551,11 +560,11 @@ __device__ __forceinline__ void value_finalize(const float4 (&vacc)[4][2], const
 // tiles / tokens are never loaded nor computed: zero-byte jobs complete their
 // barrier at once, their logits are -inf and their value operands zero.
 // -------------------------------------------------------------------------
-template <int H>
+template <int H, int IT = SUB>
 __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fast::FastArgs a) {
-    using WS = TS<H>;
+    using WS = TS<H, IT>;
     using PB = fast::P<2>;
-    constexpr int NKJ = (SUB / 32) / KT, NVJ = SUB / VT, NJ = NKJ + NVJ;
+    constexpr int NKJ = (IT / 32) / KT, NVJ = IT / VT, NJ = NKJ + NVJ;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* wbase = smem_raw + warp * WS::STRIDE;
@@ -587,15 +596,15 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     auto prefetch_item = [&](int it) {
         if (!a.prefetch || it >= a.n_items || lane != 0) return;
         const int pu = it / nper, pkk = it - pu * nper, pk = a.k_first + pkk;
-        const int Ti = min(SUB, a.body_end - pkk * SUB);
+        const int Ti = min(IT, a.body_end - pkk * IT);
         if (Ti <= 0) return;
-        bulk_prefetch_l2(c.kcodes + pu * c.k_ustride + (int64_t)pk * (SUB / 32) * PB::TILE_CODE,
+        bulk_prefetch_l2(c.kcodes + pu * c.k_ustride + (int64_t)pk * (IT / 32) * PB::TILE_CODE,
                          (uint32_t)(Ti / 32) * PB::TILE_CODE);
-        bulk_prefetch_l2(c.kpairs + pu * c.kp_ustride + (int64_t)pk * (SUB / 32) * D,
+        bulk_prefetch_l2(c.kpairs + pu * c.kp_ustride + (int64_t)pk * (IT / 32) * D,
                          (uint32_t)(Ti / 32) * D * 8);
-        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * SUB * PB::TOK_CODE,
+        bulk_prefetch_l2(c.vcodes + pu * c.v_ustride + (int64_t)pk * IT * PB::TOK_CODE,
                          (uint32_t)Ti * PB::TOK_CODE);
-        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * SUB * (D / fast::G),
+        bulk_prefetch_l2(c.vpairs + pu * c.vp_ustride + (int64_t)pk * IT * (D / fast::G),
                          (uint32_t)Ti * (D / fast::G) * 8);
     };
     int f_item = grab(), f_job = 0;
@@ -615,11 +624,11 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             uint8_t* slot = wbase + s * SLOT;
             uint64_t* bar = &bars[s];
             const int kk = a.k_first + f_k;
-            const int Ti = min(SUB, a.body_end - f_k * SUB);  // item tokens (partial last item)
+            const int Ti = min(IT, a.body_end - f_k * IT);  // item tokens (partial last item)
             fence_proxy_async_smem();
             if (f_job < NKJ) {
                 const int ntl = min(KT, max(0, Ti / 32 - f_job * KT));
-                const int64_t tile0 = (int64_t)kk * (SUB / 32) + f_job * KT;
+                const int64_t tile0 = (int64_t)kk * (IT / 32) + f_job * KT;
                 const uint32_t cb = (uint32_t)ntl * PB::TILE_CODE;
                 const uint32_t pb = (uint32_t)ntl * D * 8;
                 constexpr uint32_t qb = H * D * 4;
@@ -633,7 +642,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * H * D, qb, bar);
             } else {
                 const int ntok = min(VT, max(0, Ti - (f_job - NKJ) * VT));
-                const int64_t ts = (int64_t)kk * SUB + (f_job - NKJ) * VT;
+                const int64_t ts = (int64_t)kk * IT + (f_job - NKJ) * VT;
                 const uint32_t cb = (uint32_t)ntok * PB::TOK_CODE;
                 const uint32_t pb = (uint32_t)ntok * (D / fast::G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
@@ -677,7 +686,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     for (int item = c_next; item < a.n_items; item = c_next) {
         const int u = item / nper;
         const int k = a.k_first + (item - u * nper);
-        const int Ti = min(SUB, a.body_end - (item - u * nper) * SUB);
+        const int Ti = min(IT, a.body_end - (item - u * nper) * IT);
         float2 qv[H][2];
         float qmax = 0.f;
 #pragma unroll 1
@@ -699,17 +708,17 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
                 __syncwarp();  // qraw is reused as the bias scratch below
             }
             const int ntl = min(KT, max(0, Ti / 32 - jk * KT));
-            if (ntl) key_job<H>(slot, qv, qmax, probs, jk * KT * 32, bf, biasm, lane, sel, ntl);
+            if (ntl) key_job<H, WS::DB>(slot, qv, qmax, probs, jk * KT * 32, bf, biasm, lane, sel, ntl);
             release_slot();
         }
-        if (Ti < SUB) {  // partial item: tokens past its end get zero probability
-            for (int i = lane; i < (SUB - Ti) * H; i += 32) {
+        if (Ti < IT) {  // partial item: tokens past its end get zero probability
+            for (int i = lane; i < (IT - Ti) * H; i += 32) {
                 const int t = Ti + i / H;
                 probs[pidx<H>(t, i % H)] = -INFINITY;
             }
         }
         float2 ml[H];
-        softmax_heads<H>(probs, a.wlog ? a.wlog + (int64_t)u * H * a.l + (int64_t)k * SUB : nullptr,
+        softmax_heads<H, IT>(probs, a.wlog ? a.wlog + (int64_t)u * H * a.l + (int64_t)k * IT : nullptr,
                          a.l, ml, lane, Ti);
         float4 vacc[4][2];
 #pragma unroll
@@ -725,10 +734,10 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             uint8_t* slot = wait_slot();
             const int ntok = min(VT, max(0, Ti - jv * VT));
             if (ntok == VT)
-                value_job<H, true>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
+                value_job<H, true, WS::DB>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
                                    sel);
             else if (ntok)
-                value_job<H, false>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
+                value_job<H, false, WS::DB>(slot, probs + jv * VT * H, vacc, zs, eb_run, jv == 0, bf, lane,
                                     sel, ntok);
             if (jv == NVJ - 1) {
                 const int64_t pi = ((int64_t)u * a.n_sub + k) * H;

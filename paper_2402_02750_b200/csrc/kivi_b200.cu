@@ -341,7 +341,7 @@ struct Tuning {
     int fused_append, tail_side, small_items, small_fused, small_sub, combine_parallel;
     int tail_sub, res_sub, res_sub_body, mha_tc, pdl, tail_ctas, tail_warp_ctas, tail_last;
     int gqa_tc, gqa_partial, gqa_tail_ctas, step_graph, zero_copy_bytes, proj_split, vimma;
-    int body_prefetch, body_long_l, gqa_heads, step_fuse, body_sub;
+    int body_prefetch, body_long_l, gqa_heads, step_fuse, body_sub, gqa_item;
     void load() {
         fused_append = env_int("KIVI_FUSED_APPEND", 0);
         tail_side = env_int("KIVI_TAIL_SIDE", 1);
@@ -366,6 +366,7 @@ struct Tuning {
         gqa_heads = env_int("KIVI_GQA_HEADS", 1);
         step_fuse = env_int("KIVI_STEP_FUSE", 1);
         body_sub = env_int("KIVI_BODY_SUB", -1);
+        gqa_item = env_int("KIVI_GQA_ITEM", 256);
         zero_copy_bytes = env_int("KIVI_ZERO_COPY_BYTES", 65536);
         proj_split = env_int("KIVI_PROJ_SPLIT", 2);
         vimma = env_int("KIVI_VIMMA", 1);
@@ -907,9 +908,14 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     // body = [0, floor32(vg)) (partial last item): the CUDA-core residual items
     // then hold fewer than 32 quantized values
     const int partial = tune().gqa_partial;
+    // tensor-core body items: 256 tokens, or 384 (KIVI_GQA_ITEM=384: fewer
+    // items, C3 +2.3 %, but the tensor core's truncating fp32 accumulation runs
+    // 1.5x longer per item: rel-L2 on 50x outlier key channels 9-11e-6 vs 6-7.5e-6
+    // against the reference, too close to the 1e-5 bar; off)
+    const int git = tune().gqa_item == 384 ? 384 : 256;
     const int64_t body_end =
-        use_tc ? (partial ? (h->vg() / 32) * 32 : (h->vg() / 32 * 32) / fast::SUB * fast::SUB) : 0;
-    const int64_t nfull = ceil_div(body_end, fast::SUB);
+        use_tc ? (partial ? (h->vg() / 32) * 32 : (h->vg() / 32 * 32) / git * git) : 0;
+    const int64_t nfull = ceil_div(body_end, git);
     const int64_t ntail = ceil_div(h->l - body_end, fast::SUB);  // residual-window items
     const int64_t n_parts = nfull + ntail;                       // <= n_sub + 1
     const int64_t n_sub_cap = std::max<int64_t>(n_sub, ceil_div(h->cap, fast::SUB)) + 1;
@@ -931,7 +937,8 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
     a.part_ml = h->part_ml;
     a.wlog = weights;
     const int smem = WS::STRIDE * gqa::WARPS;
-    const int smem_tc = TWS::STRIDE * gqa_tc::WARPS;
+    const int smem_tc =
+        (git == 384 ? gqa_tc::TS<H, 384>::STRIDE : TWS::STRIDE) * gqa_tc::WARPS;
     const int key = 4 + H;
     if (h->fast_per_sm[key][2] == 0) {
         KIVI_CUDA(cudaFuncSetAttribute(gqa::attend_gqa_kernel<H>,
@@ -945,8 +952,15 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
             &per_sm, gqa::attend_gqa_kernel<H>, gqa::WARPS * 32, smem));
         h->fast_per_sm[key][2] = per_sm < 1 ? 1 : per_sm;
         KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, gqa_tc::attend_gqa_tc_kernel<H>, gqa_tc::WARPS * 32, smem_tc));
+            &per_sm, gqa_tc::attend_gqa_tc_kernel<H>, gqa_tc::WARPS * 32,
+            TWS::STRIDE * gqa_tc::WARPS));
         h->fast_per_sm[key][3] = per_sm < 1 ? 1 : per_sm;
+        const int smem_tc3 = gqa_tc::TS<H, 384>::STRIDE * gqa_tc::WARPS;
+        KIVI_CUDA(cudaFuncSetAttribute(gqa_tc::attend_gqa_tc_kernel<H, 384>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc3));
+        KIVI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, gqa_tc::attend_gqa_tc_kernel<H, 384>, gqa_tc::WARPS * 32, smem_tc3));
+        h->fast_per_sm[key][4] = per_sm < 1 ? 1 : per_sm;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     h->prof_now = h->profile && (h->profile_seq++ % h->profile_stride == 0);
@@ -997,10 +1011,15 @@ kivi_status launch_gqa(kivi_cache* h, const float* q, float* out, float* weights
         a.n_per_unit = (int)nfull;
         a.n_items = (int)(U * nfull);
         a.prefetch = tune().body_prefetch;
+        a.sub = git;
         take_work_slot(h, a);
-        const int64_t grid = std::min<int64_t>((int64_t)num_sms() * h->fast_per_sm[key][3],
-                                               ceil_div(a.n_items, gqa_tc::WARPS));
-        gqa_tc::attend_gqa_tc_kernel<H><<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
+        const int64_t grid = std::min<int64_t>(
+            (int64_t)num_sms() * h->fast_per_sm[key][git == 384 ? 4 : 3],
+            ceil_div(a.n_items, gqa_tc::WARPS));
+        if (git == 384)
+            gqa_tc::attend_gqa_tc_kernel<H, 384><<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
+        else
+            gqa_tc::attend_gqa_tc_kernel<H><<<(unsigned)grid, gqa_tc::WARPS * 32, smem_tc, st>>>(a);
         KIVI_LAUNCHED();
         h->total_launches++;
     }

@@ -592,6 +592,19 @@ def test_gqa_heads_route(cuda, bits, qpk, small, monkeypatch):
     assert ew <= 1e-5, ew
 
 
+@pytest.mark.parametrize("qpk", [2, 4])
+def test_gqa_384_token_items(cuda, qpk, monkeypatch):
+    """The tensor-core GQA body with 384-token items (KIVI_GQA_ITEM=384, off by
+    default: its longer truncating accumulation costs accuracy on outlier
+    channels), on ordinary operands across a partial last item, with weights."""
+    monkeypatch.setenv("KIVI_GQA_ITEM", "384")
+    for l0 in (1100, 1500):
+        e, ew = run_gqa((2, 32, 128, 128), U=3, qpk=qpk, l0=l0, steps=2, path="fast",
+                        seed=l0 + qpk, weights=True)
+        assert e <= 1e-5, e
+        assert ew <= 1e-5, ew
+
+
 # (kscale, vscale, qscale, key outlier channels, tolerance).  The last case
 # has log2-domain logits of magnitude ~500: one fp32 ulp there is 3e-5, so
 # even the reference's own float cast of its double logits (attention.cpp:59-62)
