@@ -146,36 +146,47 @@ __device__ __forceinline__ void value_job(uint8_t* slot, const float* p, State& 
     const int g = lane >> 2, t4 = lane & 3;
     int eprod;
     {
-        int e4[4];
+        // the four groups' exponents in every lane with two shuffles: lanes
+        // with lane % 4 == c hold group c's (ej + 90 in [0, 219]: one byte)
+        uint32_t w = (uint32_t)(ej + 90) << (8 * cg);
+        w |= __shfl_xor_sync(FULL, w, 1);
+        w |= __shfl_xor_sync(FULL, w, 2);
+        int ec[4];
+        bool grow = false;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const int ec = __shfl_sync(FULL, ej, c);
-            e4[c] = st.first ? ec : max(st.E[c], ec);
-            if (!st.first && ec > st.E[c]) {  // warp-uniform
-                // larger spans than the item's earlier jobs: this group's
-                // integer sums move to fp32 at the old scale (digit columns
-                // cannot be shifted one by one: the bits a digit column
-                // drops belong to the column below), then restart at 0
-                const float sc_old = pow2f(st.E[c] - 31);
+            ec[c] = (int)((w >> (8 * c)) & 0xFFu) - 90;
+            grow |= !st.first && ec[c] > st.E[c];
+        }
+        if (grow) {  // warp-uniform, rare
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const bool mine = 2 * e + (g >> 2) == c;
+            for (int c = 0; c < 4; ++c) {
+                if (ec[c] > st.E[c]) {
+                    // larger spans than the item's earlier jobs: this group's
+                    // integer sums move to fp32 at the old scale (digit columns
+                    // cannot be shifted one by one: the bits a digit column
+                    // drops belong to the column below), then restart at 0
+                    const float sc_old = pow2f(st.E[c] - 31);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float a, b;
-                        combine_digits(st.D[e][j], t4, a, b);
-                        if (mine) {
-                            st.F[e][j][0] = fmaf(a, sc_old, st.F[e][j][0]);
-                            st.F[e][j][1] = fmaf(b, sc_old, st.F[e][j][1]);
+                    for (int e = 0; e < 2; ++e) {
+                        const bool mine = 2 * e + (g >> 2) == c;
 #pragma unroll
-                            for (int r = 0; r < 4; ++r) st.D[e][j][r] = 0;
+                        for (int j = 0; j < 4; ++j) {
+                            float a, b;
+                            combine_digits(st.D[e][j], t4, a, b);
+                            if (mine) {
+                                st.F[e][j][0] = fmaf(a, sc_old, st.F[e][j][0]);
+                                st.F[e][j][1] = fmaf(b, sc_old, st.F[e][j][1]);
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) st.D[e][j][r] = 0;
+                            }
                         }
                     }
                 }
             }
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) st.E[c] = e4[c];
+        for (int c = 0; c < 4; ++c) st.E[c] = st.first ? ec[c] : max(st.E[c], ec[c]);
         eprod = pick4(st.E, cg);
     }
     st.first = false;
