@@ -5,12 +5,12 @@
 //         = (1/3) sum_t code_tc * (p_t * (hi - lo)_t,cg) + sum_t p_t lo_t,cg
 //
 // A = the 2-bit value codes as u8 (exact), M = 16 channels x K = 32 tokens.
-// B = x_t,cg = round(p_t (hi - lo)_t,cg 2^(31 - E_cg)) split into its four
+// B = x_t,cg = round(p_t (hi - lo)_t,cg 2^(31 - E)) split into its four
 //     bytes (digits d = 0..3, x = sum_d byte_d 256^d), N = 8 columns =
-//     (channel-group half, digit); 2^E_cg bounds the item's spans of that
-//     channel group, so x < 2^31 and the four digit products sum exactly in
-//     int32 (<= 255 * 3 * 256 per column per item).
-// The fixed point carries 31 bits below the group's largest span (p <= 1):
+//     (channel-group half, digit); 2^E bounds the item's spans (all channel
+//     groups), so x < 2^31 and the four digit products sum exactly in int32
+//     (<= 255 * 3 * 256 per column per item).
+// The fixed point carries 31 bits below the item's largest span (p <= 1):
 // its error is ~2^-31 of the largest term, below fp32 accumulation's.
 //
 // Why: the CUDA-core value loop spends one LOP3 per code (ALU pipe, half
@@ -61,16 +61,11 @@ __device__ __forceinline__ uint32_t shr4(uint32_t x) { return __umulhi(x, 1u << 
 // 2^k as a float for k in [-126, 127]
 __device__ __forceinline__ float pow2f(int k) { return __uint_as_float((uint32_t)(k + 127) << 23); }
 
-// E[i] for a run-time i without local-memory indexing
-__device__ __forceinline__ int pick4(const int (&E)[4], int i) {
-    return i == 0 ? E[0] : (i == 1 ? E[1] : (i == 2 ? E[2] : E[3]));
-}
-
 // Per-warp state of an item's value phase (registers).
 struct State {
     int D[2][4][4];   // [channel half e][M-block j][mma regs]
     float F[2][4][2]; // [e][j][row g, g + 8]: D flushed at an exponent change
-    int E[4];         // running span exponent per channel group (item)
+    int E;            // running span exponent of the item (all channel groups)
     float z;          // producer lane's share of sum_t p_t lo_t,cg (cg = lane % 4)
     bool first;
 };
@@ -136,59 +131,35 @@ __device__ __forceinline__ void value_job(uint8_t* slot, const float* p, State& 
             smax = fmaxf(smax, span[kb][i]);
             st.z = fmaf(pt[kb][i], pr.x, st.z);
         }
-    smax = fmaxf(smax, __shfl_xor_sync(FULL, smax, 4));
-    smax = fmaxf(smax, __shfl_xor_sync(FULL, smax, 8));
-    smax = fmaxf(smax, __shfl_xor_sync(FULL, smax, 16));
+    // one exponent for the job's four channel groups: a warp max (CREDUX).  A
+    // group whose spans are 2^k below the job's largest keeps 31 - k bits of
+    // fixed point, still far below the fp32 rounding it replaces.
+    smax = warp_max_redux(smax);
     // smax < 2^E; E >= -90 keeps 2^(31 - E) and 2^(E - 31) normal floats
     // (all-constant groups have smax = 0 and x = 0)
     const int ej = max((int)((__float_as_uint(smax) >> 23) & 0xFFu) - 126, -90);
-    // consumer role: lane = (g, t4); its D rows of half e belong to group 2e + g/4
+    // consumer role: lane = (g, t4)
     const int g = lane >> 2, t4 = lane & 3;
-    int eprod;
-    {
-        // the four groups' exponents in every lane with two shuffles: lanes
-        // with lane % 4 == c hold group c's (ej + 90 in [0, 219]: one byte)
-        uint32_t w = (uint32_t)(ej + 90) << (8 * cg);
-        w |= __shfl_xor_sync(FULL, w, 1);
-        w |= __shfl_xor_sync(FULL, w, 2);
-        int ec[4];
-        bool grow = false;
+    if (!st.first && ej > st.E) {  // warp-uniform, rare
+        // larger spans than the item's earlier jobs: the integer sums move to
+        // fp32 at the old scale (digit columns cannot be shifted one by one:
+        // the bits a digit column drops belong to the column below), then
+        // restart at 0
+        const float sc_old = pow2f(st.E - 31);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            ec[c] = (int)((w >> (8 * c)) & 0xFFu) - 90;
-            grow |= !st.first && ec[c] > st.E[c];
-        }
-        if (grow) {  // warp-uniform, rare
+        for (int e = 0; e < 2; ++e)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                if (ec[c] > st.E[c]) {
-                    // larger spans than the item's earlier jobs: this group's
-                    // integer sums move to fp32 at the old scale (digit columns
-                    // cannot be shifted one by one: the bits a digit column
-                    // drops belong to the column below), then restart at 0
-                    const float sc_old = pow2f(st.E[c] - 31);
+            for (int j = 0; j < 4; ++j) {
+                float a, b;
+                combine_digits(st.D[e][j], t4, a, b);
+                st.F[e][j][0] = fmaf(a, sc_old, st.F[e][j][0]);
+                st.F[e][j][1] = fmaf(b, sc_old, st.F[e][j][1]);
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const bool mine = 2 * e + (g >> 2) == c;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float a, b;
-                            combine_digits(st.D[e][j], t4, a, b);
-                            if (mine) {
-                                st.F[e][j][0] = fmaf(a, sc_old, st.F[e][j][0]);
-                                st.F[e][j][1] = fmaf(b, sc_old, st.F[e][j][1]);
-#pragma unroll
-                                for (int r = 0; r < 4; ++r) st.D[e][j][r] = 0;
-                            }
-                        }
-                    }
-                }
+                for (int r = 0; r < 4; ++r) st.D[e][j][r] = 0;
             }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st.E[c] = st.first ? ec[c] : max(st.E[c], ec[c]);
-        eprod = pick4(st.E, cg);
     }
+    st.E = st.first ? ej : max(st.E, ej);
+    const int eprod = st.E;
     st.first = false;
     const float xscale = pow2f(31 - eprod);
     __syncwarp();  // every lane has read its pairs: the region now takes the digits
@@ -247,7 +218,7 @@ __device__ __forceinline__ void finalize(const State& st, float2 ml, float* part
     for (int e = 0; e < 2; ++e) {
         const int cgc = 2 * e + (g >> 2);
         const float zc = __shfl_sync(FULL, z, cgc);
-        const float sc = pow2f(pick4(st.E, cgc) - 31);
+        const float sc = pow2f(st.E - 31);
         float v[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
