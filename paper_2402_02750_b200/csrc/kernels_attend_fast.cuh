@@ -649,6 +649,17 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
     int pend = 0;
     int c_next = f_item;    // next item for the compute loop
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
+    // the item's source addresses, advanced by a constant per job (the 64-bit
+    // unit / item arithmetic once per item instead of once per copy)
+    const uint8_t *src_kc, *src_vc;
+    const float2 *src_kp, *src_vp;
+    auto item_sources = [&]() {
+        src_kc = c.kcodes + f_u * c.k_ustride + (int64_t)f_k * (BS / 32) * PB::TILE_CODE;
+        src_kp = c.kpairs + f_u * c.kp_ustride + (int64_t)f_k * (BS / 32) * D;
+        src_vc = c.vcodes + f_u * c.v_ustride + (int64_t)f_k * BS * PB::TOK_CODE;
+        src_vp = c.vpairs + f_u * c.vp_ustride + (int64_t)f_k * BS * (D / G);
+    };
+    item_sources();
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
@@ -657,24 +668,22 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             uint64_t* bar = &bars[s];
             fence_proxy_async_smem();
             if (f_job < NKJ) {
-                const int64_t tile0 = (int64_t)f_k * (BS / 32) + f_job * PB::KQ_TILES;
                 constexpr uint32_t cb = PB::KQ_TILES * PB::TILE_CODE;
                 constexpr uint32_t pb = PB::KQ_TILES * D * 8;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? D * 4 : 0));
-                bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE, cb,
-                                     bar, policy);
-                bulk_g2s_evict_first(slot + cb, c.kpairs + f_u * c.kp_ustride + tile0 * D, pb, bar,
-                                     policy);
+                bulk_g2s_evict_first(slot, src_kc, cb, bar, policy);
+                bulk_g2s_evict_first(slot + cb, src_kp, pb, bar, policy);
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * D, D * 4, bar);
+                src_kc += cb;
+                src_kp += PB::KQ_TILES * D;
             } else {
-                const int64_t ts = (int64_t)f_k * BS + (f_job - NKJ) * PB::VQ_TOK;
                 constexpr uint32_t cb = PB::VQ_TOK * PB::TOK_CODE;
                 constexpr uint32_t pb = PB::VQ_TOK * (D / G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
-                bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb, bar,
-                                     policy);
-                bulk_g2s_evict_first(slot + cb, c.vpairs + f_u * c.vp_ustride + ts * (D / G), pb, bar,
-                                     policy);
+                bulk_g2s_evict_first(slot, src_vc, cb, bar, policy);
+                bulk_g2s_evict_first(slot + cb, src_vp, pb, bar, policy);
+                src_vc += cb;
+                src_vp += PB::VQ_TOK * (D / G);
             }
         }
         if (++f_job == NJ) {
@@ -687,6 +696,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) attend_body_kernel(FastArgs a) 
             }
             f_u = f_item / nper;
             f_k = f_item - f_u * nper;
+            item_sources();
         }
     };
     issue_next(0);
