@@ -617,42 +617,52 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
     int pend = 0;
     int c_next = f_item;
     int f_u = f_item / nper, f_k = f_item - f_u * nper;
+    // the item's source addresses and token count, once per item; the
+    // addresses advance by a constant per job
+    const uint8_t *src_kc, *src_vc;
+    const float2 *src_kp, *src_vp;
+    int f_ti;
+    auto item_sources = [&]() {
+        const int64_t kk = a.k_first + f_k;
+        f_ti = min(IT, a.body_end - f_k * IT);  // item tokens (partial last item)
+        src_kc = c.kcodes + f_u * c.k_ustride + kk * (IT / 32) * PB::TILE_CODE;
+        src_kp = c.kpairs + f_u * c.kp_ustride + kk * (IT / 32) * D;
+        src_vc = c.vcodes + f_u * c.v_ustride + kk * IT * PB::TOK_CODE;
+        src_vp = c.vpairs + f_u * c.vp_ustride + kk * IT * (D / fast::G);
+    };
+    item_sources();
     auto issue_next = [&](int s) {
         if (f_item >= a.n_items) return;
         if (lane == 0) {
             if (KIVI_DEFER_CLAIM && f_job == 0 && f_ahead < a.n_items) pend = atomicAdd(a.work, 1);
             uint8_t* slot = wbase + s * SLOT;
             uint64_t* bar = &bars[s];
-            const int kk = a.k_first + f_k;
-            const int Ti = min(IT, a.body_end - f_k * IT);  // item tokens (partial last item)
+            const int Ti = f_ti;
             fence_proxy_async_smem();
             if (f_job < NKJ) {
                 const int ntl = min(KT, max(0, Ti / 32 - f_job * KT));
-                const int64_t tile0 = (int64_t)kk * (IT / 32) + f_job * KT;
                 const uint32_t cb = (uint32_t)ntl * PB::TILE_CODE;
                 const uint32_t pb = (uint32_t)ntl * D * 8;
                 constexpr uint32_t qb = H * D * 4;
                 mbar_arrive_expect_tx(bar, cb + pb + (f_job == 0 ? qb : 0));
                 if (ntl) {
-                    bulk_g2s_evict_first(slot, c.kcodes + f_u * c.k_ustride + tile0 * PB::TILE_CODE,
-                                         cb, bar, policy);
-                    bulk_g2s_evict_first(slot + KT * PB::TILE_CODE,
-                                         c.kpairs + f_u * c.kp_ustride + tile0 * D, pb, bar, policy);
+                    bulk_g2s_evict_first(slot, src_kc, cb, bar, policy);
+                    bulk_g2s_evict_first(slot + KT * PB::TILE_CODE, src_kp, pb, bar, policy);
                 }
                 if (f_job == 0) bulk_g2s(qraw, a.q + (int64_t)f_u * H * D, qb, bar);
+                src_kc += KT * PB::TILE_CODE;
+                src_kp += KT * D;
             } else {
                 const int ntok = min(VT, max(0, Ti - (f_job - NKJ) * VT));
-                const int64_t ts = (int64_t)kk * IT + (f_job - NKJ) * VT;
                 const uint32_t cb = (uint32_t)ntok * PB::TOK_CODE;
                 const uint32_t pb = (uint32_t)ntok * (D / fast::G) * 8;
                 mbar_arrive_expect_tx(bar, cb + pb);
                 if (ntok) {
-                    bulk_g2s_evict_first(slot, c.vcodes + f_u * c.v_ustride + ts * PB::TOK_CODE, cb,
-                                         bar, policy);
-                    bulk_g2s_evict_first(slot + VT * PB::TOK_CODE,
-                                         c.vpairs + f_u * c.vp_ustride + ts * (D / fast::G), pb, bar,
-                                         policy);
+                    bulk_g2s_evict_first(slot, src_vc, cb, bar, policy);
+                    bulk_g2s_evict_first(slot + VT * PB::TOK_CODE, src_vp, pb, bar, policy);
                 }
+                src_vc += VT * PB::TOK_CODE;
+                src_vp += VT * (D / fast::G);
             }
         }
         if (++f_job == NJ) {
@@ -665,6 +675,7 @@ __global__ void __launch_bounds__(WARPS * 32, MIN_CTAS) attend_gqa_tc_kernel(fas
             }
             f_u = f_item / nper;
             f_k = f_item - f_u * nper;
+            item_sources();
         }
     };
     issue_next(0);
