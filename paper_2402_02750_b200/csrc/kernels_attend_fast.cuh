@@ -1191,17 +1191,17 @@ __global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ 
 // One layer's K5 merge fused with the NEXT layer's append (a multi-layer
 // decode step on one stream): blocks [0, n_comb) merge layer i's partials
 // exactly as combine_kernel (they wait for the attend before them); blocks
-// [n_comb, n_comb + n_app) append layer i+1's token rows, one warp per unit
-// (append_fast_kernel), and the rest quantize layer i+1's complete key tiles
-// (append_flush_fast_kernel).  The append touches only layer i+1's cache,
+// [n_comb, ...) append layer i+1's token rows, one warp per unit
+// (append_fast_kernel; a step that completes key tiles quantizes them in a
+// separate append_flush_fast_kernel launch, whose 32-value registers would
+// otherwise cut this kernel's occupancy).  The append touches only layer i+1's cache,
 // which no kernel in flight reads, so it runs beside the merge instead of as
 // its own launch after it.
 template <int B>
 __global__ void __launch_bounds__(128) combine_append_kernel(
     const float* __restrict__ part_o, const float2* __restrict__ part_ml, int n_sub,
     float* __restrict__ out, int cmode, int64_t n_rows, int n_comb, CacheDev cn,
-    const float* __restrict__ tk, const float* __restrict__ tv, int64_t l_next, int n_app, int tl0,
-    int ntl) {
+    const float* __restrict__ tk, const float* __restrict__ tv, int64_t l_next) {
     pdl_trigger();  // the next layer's attend may be scheduled (it waits for all of this)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if ((int)blockIdx.x < n_comb) {
@@ -1218,13 +1218,8 @@ __global__ void __launch_bounds__(128) combine_append_kernel(
             combine_row_serial(part_o, part_ml, n_sub, u * n_sub, 1, out + u * D, nullptr);
         return;
     }
-    const int b = (int)blockIdx.x - n_comb;
-    if (b < n_app) {
-        const int64_t u = (int64_t)b * 4 + warp;
-        if (u < cn.n_units) append_unit_fast<B, false>(cn, tk, tv, l_next, u, lane);
-        return;
-    }
-    flush_key_group<B>(cn, tk, l_next, (int64_t)(b - n_app) * 4 + warp, tl0, ntl, lane);
+    const int64_t u = (int64_t)((int)blockIdx.x - n_comb) * 4 + warp;
+    if (u < cn.n_units) append_unit_fast<B, false>(cn, tk, tv, l_next, u, lane);
 }
 
 // Optional weights: w_t = 2^(logit2_t - M) / L, in place over the wlog buffer.

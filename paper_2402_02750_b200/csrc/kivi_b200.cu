@@ -1763,14 +1763,21 @@ static kivi_status decode_layers_fused(kivi_cache* const* caches, int32_t n_laye
             int tl0, ntl;
             key_tiles_due(hn, &tl0, &ntl);
             const int n_app = (int)ceil_div(U, 4);
-            const int n_fl = ntl > 0 ? (int)ceil_div(U * ntl * 128, 128) : 0;
-            KIVI_CUDA(launch_pdl(fast::combine_append_kernel<B>, dim3((unsigned)(n_comb + n_app + n_fl)),
+            KIVI_CUDA(launch_pdl(fast::combine_append_kernel<B>, dim3((unsigned)(n_comb + n_app)),
                                  dim3(fast::D), 0, st, (const float*)h->part_o,
                                  (const float2*)h->part_ml, n_sub, out + i * krow, cmode, (int64_t)U,
                                  n_comb, hn->dev, t_k + (i + 1) * krow, t_v + (i + 1) * krow,
-                                 (int64_t)hn->l, n_app, tl0, ntl));
+                                 (int64_t)hn->l));
             KIVI_LAUNCHED();
             h->total_launches++;
+            if (ntl > 0) {  // complete key tiles of layer i+1 (every 32 steps)
+                const unsigned fgrid = (unsigned)ceil_div(U * ntl * 128, 256);
+                append_flush_fast_kernel<B><<<fgrid, 256, 0, st>>>(
+                    hn->dev, t_k + (i + 1) * krow, t_v + (i + 1) * krow, hn->l, 0, tl0, ntl,
+                    QStage{nullptr, nullptr, 0});
+                KIVI_LAUNCHED();
+                hn->total_launches++;
+            }
             append_bookkeeping(hn);
         } else {
             KIVI_CUDA(launch_pdl(fast::combine_kernel, dim3((unsigned)n_comb), dim3(fast::D), 0, st,
