@@ -34,6 +34,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attn tokens/s and achieved HBM GB/s vs roofline, 1/2/4/8 B200"
+OUTLIER_CHANNELS = [1, 17, 40]  # analysis.hpp:59-61
+
+
+def data_note(args):
+    dist = "N(0,1)" if args.data == "normal" else "uniform(-1,1)"
+    out = ", key channels {1,17,40} x50" if args.outliers else ""
+    return f"synthetic ({dist} K/V/q{out}, generated on device; random-init, no checkpoint)"
 
 # name -> (layers, kv_heads, batch, ctx, bits, q_per_kv, description)
 CONFIGS = {
@@ -322,7 +329,8 @@ def run_reference_arm(args):
         # the timed step IS the bounded sample: its measured duration
         "ms_per_step": secs / max(args.steps, 1) * 1e3, "higher_is_better": True,
         "scaling": scaling,
-        "vs_baseline": None, "dtype": "f32/f64 (reference CPU)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32/f64 (reference CPU)",
+        "data": "synthetic (uniform(-1,1) from the oracle's counter RNG; CPU time is data-independent)",
         "config": cfg,
         "sampled_units": units, "sample_seconds": secs,
         "ms_per_full_step_extrapolated": step_s * 1e3,
@@ -425,12 +433,23 @@ def run_ours(args):
     sample_units = sorted({(i * U) // 8 + (i % 3) for i in range(8)} & set(range(U)))
     prompts = {}
 
+    def fill(t, keys=False):
+        """SURVEY §8d inputs: N(0, 1) (or uniform(-1, 1)); --outliers scales key
+        channels {1, 17, 40} by 50 (analysis.hpp:59-61): scales change, bytes do not."""
+        if args.data == "normal":
+            t.normal_(0.0, 1.0, generator=gen)
+        else:
+            t.uniform_(-1.0, 1.0, generator=gen)
+        if keys and args.outliers:
+            t[..., OUTLIER_CHANNELS] *= 50.0
+        return t
+
     def rebuild():
         """Every layer back to l0 tokens, from the same seeded draws."""
         for ly in range(layers):
             gen.manual_seed(1234 + 1000 * rank + ly)
-            kbuf.uniform_(-1.0, 1.0, generator=gen)
-            vbuf.uniform_(-1.0, 1.0, generator=gen)
+            fill(kbuf, keys=True)
+            fill(vbuf)
             caches[ly].prefill(kbuf, vbuf)
             if ly == 0 and do_parity and not prompts:
                 for u in sample_units:
@@ -440,9 +459,9 @@ def run_ours(args):
     # per-step inputs resident in HBM (a pool of 2 sets per layer, cycled)
     pool = 2
     gen.manual_seed(99 + rank)
-    qs = torch.empty((pool, layers, U, qpk, D), device=dev).uniform_(-1, 1, generator=gen)
-    ks = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
-    vs = torch.empty((pool, layers, U, D), device=dev).uniform_(-1, 1, generator=gen)
+    qs = fill(torch.empty((pool, layers, U, qpk, D), device=dev))
+    ks = fill(torch.empty((pool, layers, U, D), device=dev), keys=True)
+    vs = fill(torch.empty((pool, layers, U, D), device=dev))
     outs = torch.empty((layers, U, qpk, D), device=dev)
 
     stack = kb.LayerStack(caches)  # one C-ABI call per step: the layer loop is native
@@ -678,7 +697,7 @@ def run_ours(args):
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (uniform(-1,1) K/V/q generated on device)",
+            "data": data_note(args),
             "config": config,
             "l2": l2_note,
             "hbm_gbs_per_gpu_step": alg_bytes / elapsed / 1e9,
@@ -718,6 +737,10 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
     ap.add_argument("--bits", type=int, default=0, choices=[0, 2, 4],
                     help="override the config's bit width (C4 sweeps 2 and 4)")
+    ap.add_argument("--data", choices=["normal", "uniform"], default="normal",
+                    help="synthetic K/V/q distribution (SURVEY §8d: N(0, 1))")
+    ap.add_argument("--outliers", action="store_true",
+                    help="key channels {1, 17, 40} x 50 (the reference's outlier analysis)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--gather", action="store_true",
