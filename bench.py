@@ -379,8 +379,9 @@ def percentiles(xs):
     def p(f):
         return ys[min(len(ys) - 1, max(0, int(math.ceil(f * len(ys))) - 1))]
 
+    # at_ctx: the last timed step, the one at l = ctx
     return {"p50": p(0.5), "p90": p(0.9), "p99": p(0.99), "max": ys[-1],
-            "mean": sum(ys) / len(ys), "n": len(ys)}
+            "mean": sum(ys) / len(ys), "n": len(ys), "at_ctx": xs[-1]}
 
 
 def run_ours(args):
