@@ -11,6 +11,10 @@
 #ifndef KIVI_DEFER_CLAIM
 #define KIVI_DEFER_CLAIM 0
 #endif
+// Key-tile flush: two streaming passes over the ring rows (see flush_key_group).
+#ifndef KIVI_FLUSH_STREAM
+#define KIVI_FLUSH_STREAM 1
+#endif
 
 namespace kivi_b200 {
 

@@ -374,30 +374,177 @@ __global__ void __launch_bounds__(256) append_fast_kernel(CacheDev c, const floa
     append_unit_fast<B, false>(c, tk, tv, l, u, lane);
 }
 
-// Flush warp fw of an early key-tile quantisation: (unit, tile tl0 + ..,
-// 32-channel slice) = one group per lane (see append_flush_fast_kernel).
+#ifndef KIVI_FLUSH_GPT
+#define KIVI_FLUSH_GPT 1
+#endif
+#if KIVI_FLUSH_STREAM
+constexpr int FLUSH_GPT = KIVI_FLUSH_GPT;  // key groups (channels) per flush thread
+#else
+constexpr int FLUSH_GPT = 1;
+#endif
+
+template <int N>
+__device__ __forceinline__ void load_vec(const float* p, float (&v)[N]) {
+    if constexpr (N == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else if constexpr (N == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = *p;
+    }
+}
+
+// Flush warp fw of an early key-tile quantisation.
+// KIVI_FLUSH_STREAM: lane = FLUSH_GPT consecutive channels (groups) of one
+// (unit, tile); a warp covers 32 * FLUSH_GPT channels, every ring row one
+// coalesced load per warp.  Two streaming passes over the 32 rows (min / max,
+// then codes) instead of 32 values per group held in registers; per value ~9
+// instructions: FMNMX pairs (+0 / -0 re-resolved in order only when an end
+// is zero, as minmax_first_last), the code y = fma(v - lo, r, 1.5 * 2^23)
+// read from y's mantissa (one LOP3), the near-tie test on
+// fma(v - lo, r, -rint) (fewer roundings than quant_code_fast's x, so its tie
+// margin still covers the error) and one flag per group instead of a redo
+// mask: a group with a near-tie value (rare) is re-coded value by value with
+// quant_code.  Codes are the reference's either way.
+// Otherwise: one group per lane, 32 values in registers (key_group_fast).
 template <int B>
 __device__ __forceinline__ void flush_key_group(const CacheDev& c, const float* __restrict__ tk,
                                                 int64_t l, int64_t fw, int tl0, int ntl, int lane) {
     constexpr int D = 128, G = 32;
+    const int last = (int)(l % c.R);  // ring row of token l (written by this launch)
+#if KIVI_FLUSH_STREAM
+    constexpr int NG = FLUSH_GPT, WPT = D / (32 * NG);  // warps per (unit, tile)
+    const int64_t u = fw / (ntl * WPT);
+    if (u >= c.n_units) return;
+    const int rem = (int)(fw % (ntl * WPT));
+    const int tl = tl0 + rem / WPT;
+    const int ch = (rem % WPT) * 32 * NG + lane * NG;
+    const float* col = c.kring + u * c.ring_ustride + (int64_t)tl * G * D + ch;
+    // token l is the last row of the tile that completes at this step; its ring
+    // row may still be in flight from the append blocks of this launch
+    const bool own = tk != nullptr && last == tl * G + (G - 1);
+    float xl[NG];
+    if (own) {
+        load_vec<NG>(tk + u * D + ch, xl);
+    } else {
+        load_vec<NG>(col + (int64_t)(G - 1) * D, xl);
+    }
+    auto ld = [&](int i, float (&v)[NG]) {
+        if (i == G - 1) {
+#pragma unroll
+            for (int j = 0; j < NG; ++j) v[j] = xl[j];
+        } else {
+            load_vec<NG>(col + (int64_t)i * D, v);
+        }
+    };
+    float lo[NG], hi[NG];
+    {
+        float v[NG];
+        ld(0, v);
+#pragma unroll
+        for (int j = 0; j < NG; ++j) lo[j] = hi[j] = v[j];
+    }
+#pragma unroll
+    for (int i = 1; i < G; ++i) {
+        float v[NG];
+        ld(i, v);
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            lo[j] = fminf(lo[j], v[j]);
+            hi[j] = fmaxf(hi[j], v[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        if (lo[j] == 0.0f || hi[j] == 0.0f) {  // +0 / -0: first zero for lo, last for hi
+            float zf = 0.0f, zl = 0.0f;
+            bool seen = false;
+#pragma unroll 1
+            for (int i = 0; i < G; ++i) {
+                float v[NG];
+                ld(i, v);
+                if (v[j] == 0.0f) {
+                    if (!seen) zf = v[j];
+                    zl = v[j];
+                    seen = true;
+                }
+            }
+            if (lo[j] == 0.0f) lo[j] = zf;
+            if (hi[j] == 0.0f) hi[j] = zl;
+        }
+    }
+    asm volatile("" ::: "memory");  // re-read the rows below; do not keep them live
+    CodeCtx cc[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) cc[j] = make_code_ctx(lo[j], hi[j], (1 << B) - 1);
+    constexpr int CPW = 32 / B;
+    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+    uint32_t w[NG][B];
+    bool near_tie[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        near_tie[j] = false;
+#pragma unroll
+        for (int k = 0; k < B; ++k) w[j][k] = 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        float v[NG];
+        ld(i, v);
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            const float t = __fsub_rn(v[j], cc[j].lo);
+            const float y = __fmaf_rn(t, cc[j].r, MAGIC);
+            const float d = __fmaf_rn(t, cc[j].r, -__fsub_rn(y, MAGIC));
+            near_tie[j] |= !(fabsf(d) < cc[j].tie);
+            w[j][i / CPW] += ((uint32_t)__float_as_int(y) & (uint32_t)cc[j].maxc) << (B * (i % CPW));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        if (near_tie[j]) {
+#pragma unroll 1
+            for (int k = 0; k < B; ++k) {
+                uint32_t word = 0;
+#pragma unroll 1
+                for (int i = 0; i < CPW; ++i) {
+                    float v[NG];
+                    ld(k * CPW + i, v);
+                    word |= quant_code(cc[j], v[j]) << (B * i);
+                }
+                w[j][k] = word;
+            }
+        }
+    }
+    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) store_key_words<B>(dst + j * B, w[j]);
+    float2* pd = c.kpairs + u * c.kp_ustride + g;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) pd[j] = make_float2(lo[j], hi[j]);
+#else
     const int64_t u = fw / (ntl * (D / 32));
     if (u >= c.n_units) return;
     const int rem = (int)(fw % (ntl * (D / 32)));
     const int tl = tl0 + rem / (D / 32);
     const int ch = (rem % (D / 32)) * 32 + lane;
     const float* kring = c.kring + u * c.ring_ustride;
-    const int last = (int)(l % c.R);  // ring row of token l (written by this launch)
+    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
+    uint32_t w[B];
+    float2 lh;
     float x[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         const int r = tl * G + i;
         x[i] = (r == last && tk) ? __ldg(tk + u * D + ch) : kring[(int64_t)r * D + ch];
     }
-    uint32_t w[B];
-    const float2 lh = key_group_fast<B>(x, w);
-    const int64_t g = ((l - l % c.R) / G + tl) * D + ch;
+    lh = key_group_fast<B>(x, w);
     store_key_words<B>(reinterpret_cast<uint32_t*>(c.kcodes + u * c.k_ustride) + g * B, w);
     c.kpairs[u * c.kp_ustride + g] = lh;
+#endif
 }
 
 // Append plus early key-tile quantisation: blocks [0, n_app) append one unit
@@ -416,7 +563,10 @@ __device__ __forceinline__ void flush_key_group(const CacheDev& c, const float* 
 // concurrently; with t_k == NULL (n_app = 0: the projection kernel already
 // wrote the row) from the ring.
 template <int B>
-__global__ void __launch_bounds__(256) append_flush_fast_kernel(CacheDev c,
+#ifndef KIVI_FLUSH_MINB
+#define KIVI_FLUSH_MINB 1
+#endif
+__global__ void __launch_bounds__(256, KIVI_FLUSH_MINB) append_flush_fast_kernel(CacheDev c,
                                                                 const float* __restrict__ tk,
                                                                 const float* __restrict__ tv,
                                                                 int64_t l, int n_app, int tl0,

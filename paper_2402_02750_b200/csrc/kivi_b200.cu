@@ -1365,7 +1365,7 @@ static kivi_status append_launch(kivi_cache* h, const float* t_k, const float* t
         key_tiles_due(h, &tl0, &ntl);
         if (ntl > 0) {
             // complete key tiles: extra blocks quantize them, one thread per group
-            const int64_t groups = h->n_units * ntl * 128;
+            const int64_t groups = h->n_units * ntl * (128 / FLUSH_GPT);
             const unsigned fgrid = (unsigned)ceil_div(groups, 256);
             if (cf.bits == 2)
                 append_flush_fast_kernel<2><<<grid + fgrid, 256, 0, st>>>(h->dev, t_k, t_v, h->l,
@@ -1771,7 +1771,7 @@ static kivi_status decode_layers_fused(kivi_cache* const* caches, int32_t n_laye
             KIVI_LAUNCHED();
             h->total_launches++;
             if (ntl > 0) {  // complete key tiles of layer i+1 (every 32 steps)
-                const unsigned fgrid = (unsigned)ceil_div(U * ntl * 128, 256);
+                const unsigned fgrid = (unsigned)ceil_div(U * ntl * (128 / FLUSH_GPT), 256);
                 append_flush_fast_kernel<B><<<fgrid, 256, 0, st>>>(
                     hn->dev, t_k + (i + 1) * krow, t_v + (i + 1) * krow, hn->l, 0, tl0, ntl,
                     QStage{nullptr, nullptr, 0});
@@ -2250,7 +2250,7 @@ kivi_status kivi_proj_append(kivi_proj* p, kivi_cache* h, const float* x, int64_
     key_tiles_due(h, &tl0, &ntl);
     if (ntl > 0) {
         // complete key tiles of this step: the projection wrote token l into the ring
-        const int64_t groups = h->n_units * ntl * 128;
+        const int64_t groups = h->n_units * ntl * (128 / FLUSH_GPT);
         const unsigned fgrid = (unsigned)ceil_div(groups, 256);
         if (cf.bits == 2)
             append_flush_fast_kernel<2><<<fgrid, 256, 0, st>>>(h->dev, nullptr, nullptr, h->l, 0,
