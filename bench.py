@@ -622,7 +622,7 @@ def run_ours(args):
                        "pinned host buffers, copies in the timed region, returns with the "
                        "step's outputs on the host)",
                "step_graph": dict(kb.step_graph_stats(local),
-                                  enabled=bool(int(os.environ.get("KIVI_STEP_GRAPH", "0"))))}
+                                  mode=os.environ.get("KIVI_STEP_GRAPH", "auto (single-layer steps)"))}
         seq_used = [(hk[j % pool, 0].numpy(), hv[j % pool, 0].numpy(), hq[j % pool, 0].numpy())
                     for j in range(warmup + steps)]
         last_out = ho[0].numpy().copy()

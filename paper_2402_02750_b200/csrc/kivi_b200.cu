@@ -360,7 +360,7 @@ struct Tuning {
         gqa_tc = env_int("KIVI_GQA_TC", 1);
         gqa_partial = env_int("KIVI_GQA_PARTIAL", 1);
         gqa_tail_ctas = env_int("KIVI_GQA_TAIL_CTAS", 8);
-        step_graph = env_int("KIVI_STEP_GRAPH", 0);
+        step_graph = env_int("KIVI_STEP_GRAPH", -1);  // -1: single-layer host steps only
         body_prefetch = env_int("KIVI_BODY_PREFETCH", 0);
         body_long_l = env_int("KIVI_BODY_LONG_L", 16384);
         gqa_heads = env_int("KIVI_GQA_HEADS", 1);
@@ -1985,7 +1985,11 @@ kivi_status kivi_decode_layers_host(kivi_cache* const* caches, int32_t n_layers,
     };
     bool profiling = false;
     for (int32_t i = 0; i < n_layers; ++i) profiling |= caches[i]->profile;
-    if (tune().step_graph && st != nullptr && !profiling && !grows) {
+    // per-step CUDA graph: on by default for one layer (C1 e2e 28.8-29.5k vs
+    // 27.3-27.6k tokens/s), off for many (capturing 32 layers costs more host
+    // time than the replay saves: C2 e2e 7,526-7,561 vs 7,661-7,675)
+    const bool graph = tune().step_graph > 0 || (tune().step_graph < 0 && n_layers == 1);
+    if (graph && st != nullptr && !profiling && !grows) {
         // The partial-result buffers must already exist (an allocation inside
         // a capture invalidates it): the first call of a cache runs directly.
         bool warm = true;

@@ -911,13 +911,20 @@ def test_decode_layers_equals_per_layer(cuda, graph, qpk, U, l0, monkeypatch):
                 assert a[key].tobytes() == b[key].tobytes() == c[key].tobytes(), (ly, u, key)
 
 
+@pytest.mark.parametrize("on_stream", [False, True])
 @pytest.mark.parametrize("pinned", [True, False])
 @pytest.mark.parametrize("qpk,U,l0", [(1, 32, 4000), (4, 8, 900)])
-def test_decode_layers_host_single_layer_zero_copy(cuda, pinned, qpk, U, l0, monkeypatch):
+def test_decode_layers_host_single_layer_zero_copy(cuda, pinned, qpk, U, l0, on_stream,
+                                                   monkeypatch):
     """One layer through kivi_decode_layers_host: with pinned buffers the
     append reads the key/value rows and the merge writes the outputs across
     PCIe (zero-copy); pageable buffers take the copy path.  Both equal
-    kivi_decode on device rows bit for bit, across a key flush."""
+    kivi_decode on device rows bit for bit, across a key flush.  On a stream
+    of its own the step is replayed as a CUDA graph by default (single-layer
+    steps, KIVI_STEP_GRAPH unset)."""
+    monkeypatch.delenv("KIVI_STEP_GRAPH", raising=False)
+    stream = torch.cuda.Stream() if on_stream else None
+    replayed0 = kb.step_graph_stats()["replayed"]
     rng = np.random.default_rng(90 + U + qpk)
     d = 128
     cfg = kb.CacheConfig(2, 32, 128, d)
@@ -934,9 +941,17 @@ def test_decode_layers_host_single_layer_zero_copy(cuda, pinned, qpk, U, l0, mon
         hq.copy_(torch.from_numpy(q))
         hk.copy_(torch.from_numpy(tk))
         hv.copy_(torch.from_numpy(tv))
-        sh.decode_host(hq, hk, hv, ho, q_per_kv=qpk)
+        if stream is None:
+            sh.decode_host(hq, hk, hv, ho, q_per_kv=qpk)
+        else:
+            with torch.cuda.stream(stream):
+                sh.decode_host(hq, hk, hv, ho, q_per_kv=qpk, stream=stream)
         assert ho.numpy()[0].tobytes() == want.tobytes(), step
     torch.cuda.synchronize()
+    stats = kb.step_graph_stats()
+    assert stats["capture_failed"] == 0
+    if on_stream:
+        assert stats["replayed"] > replayed0, stats
     for u in (0, U - 1):
         a, b = ref.export_unit(u), host.export_unit(u)
         for key in a:
