@@ -93,6 +93,22 @@ __device__ __forceinline__ uint32_t quant_code_fast(const CodeCtx& c, float v, b
     return (uint32_t)min(max(__float_as_int(y) - 0x4B400000, 0), c.maxc);
 }
 
+// The same decision with one FFMA: y = fma(v - lo, r, 1.5 * 2^23) rounds the
+// exact product (v - lo) * r to the nearest even integer in its mantissa (one
+// LOP3 reads the code), and d = fma(v - lo, r, -rint) is its distance to that
+// integer; fewer roundings than quant_code_fast's x, so the same tie margin
+// covers the error.  near_tie |= the decision needs the exact path (NaN r or
+// inputs included); the caller then re-codes the group with quant_code.  The
+// returned code is only meaningful when near_tie stays false.
+__device__ __forceinline__ uint32_t quant_code_fma(const CodeCtx& c, float v, bool& near_tie) {
+    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+    const float t = __fsub_rn(v, c.lo);
+    const float y = __fmaf_rn(t, c.r, MAGIC);
+    const float d = __fmaf_rn(t, c.r, -__fsub_rn(y, MAGIC));
+    near_tie |= !(fabsf(d) < c.tie);
+    return (uint32_t)__float_as_int(y) & (uint32_t)c.maxc;
+}
+
 __device__ __forceinline__ uint32_t quant_code(const CodeCtx& c, float v) {
     bool exact;
     const uint32_t q = quant_code_fast(c, v, exact);

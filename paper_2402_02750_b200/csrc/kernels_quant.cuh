@@ -480,7 +480,6 @@ __device__ __forceinline__ void flush_key_group(const CacheDev& c, const float* 
 #pragma unroll
     for (int j = 0; j < NG; ++j) cc[j] = make_code_ctx(lo[j], hi[j], (1 << B) - 1);
     constexpr int CPW = 32 / B;
-    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
     uint32_t w[NG][B];
     bool near_tie[NG];
 #pragma unroll
@@ -495,11 +494,7 @@ __device__ __forceinline__ void flush_key_group(const CacheDev& c, const float* 
         ld(i, v);
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
-            const float t = __fsub_rn(v[j], cc[j].lo);
-            const float y = __fmaf_rn(t, cc[j].r, MAGIC);
-            const float d = __fmaf_rn(t, cc[j].r, -__fsub_rn(y, MAGIC));
-            near_tie[j] |= !(fabsf(d) < cc[j].tie);
-            w[j][i / CPW] += ((uint32_t)__float_as_int(y) & (uint32_t)cc[j].maxc) << (B * (i % CPW));
+            w[j][i / CPW] += quant_code_fma(cc[j], v[j], near_tie[j]) << (B * (i % CPW));
         }
     }
 #pragma unroll
