@@ -2,7 +2,7 @@ import os, sys
 sys.path.insert(0, "/root/repo/tests"); sys.path.insert(0, "/root/repo")
 import test_gpu_parity as t
 import paper_2402_02750_b200 as kb
-for item in ("256", "384"):
+for item in os.environ.get("ITEMS", "256 384").split():
     os.environ["KIVI_GQA_ITEM"] = item
     kb.reload_tuning()
     for qpk in (2, 4):
